@@ -1,0 +1,287 @@
+// kernel_aux.cu -- everything around the hash kernels: device-side bucketing of
+// variable-length batches, the synthetic workload generators, and the raw
+// permutation test hook.
+#include "kernels.cuh"
+#include "keccak_f1600.cuh"
+
+namespace b200sha3 {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Keccak-f[1600] on raw states: permute_1600 (proj/core/src/keccak.cpp:245-277)
+// with nothing around it; pins the device permutation against the 200-byte KAT
+// of proj/tests/test_keccak.cpp:456-466.
+__global__ void __launch_bounds__(128) permute_kernel(uint64_t* states, uint64_t count) {
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (tid >= count) return;
+  uint2* s = reinterpret_cast<uint2*>(states + 25 * tid);
+  State a;
+#pragma unroll
+  for (int i = 0; i < 25; ++i) {
+    const uint2 v = s[i];
+    a.lo[i] = v.x;
+    a.hi[i] = v.y;
+  }
+  keccak_f1600<2, 0u>(a);
+#pragma unroll
+  for (int i = 0; i < 25; ++i) s[i] = make_uint2(a.lo[i], a.hi[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Bucketing.  The reference balances uneven messages by handing small chunks
+// to a thread pool (plan_partition, proj/core/src/batch.cpp:46-62).  On the
+// GPU the cost of an uneven batch is warp divergence: 32 threads run as long
+// as the longest message among them.  We therefore process messages in order
+// of their absorb-block count, heaviest first, so that the threads of a warp
+// run (nearly) the same number of permutations.
+//
+// Key: the block count itself below 128, then 16 sub-bins per power of two
+// (<= 6.25 % spread inside a bin), clamped to 255 keys; stored inverted so
+// that key 0 is the heaviest bin.
+__device__ __forceinline__ uint32_t bucket_key(uint64_t len, uint32_t rate_bytes) {
+  const uint64_t blocks = len / rate_bytes + 1u;
+  uint32_t key;
+  if (blocks < 128u) {
+    key = static_cast<uint32_t>(blocks);
+  } else {
+    const int e = 63 - __clzll(static_cast<long long>(blocks));  // >= 7
+    const uint32_t frac = static_cast<uint32_t>(blocks >> (e - 4)) & 15u;
+    key = 128u + static_cast<uint32_t>(e - 7) * 16u + frac;
+    if (key > 255u) key = 255u;
+  }
+  return 255u - key;
+}
+
+constexpr int kBucketThreads = 256;
+constexpr int kBucketItems = 8;  // messages per thread
+
+// scratch layout: [0,256) histogram / bin base, [256,512) running cursor,
+// [512] unused.
+__global__ void __launch_bounds__(kBucketThreads)
+bucket_histogram_kernel(const uint64_t* __restrict__ offsets,
+                        const uint64_t* __restrict__ lengths, uint32_t count,
+                        uint32_t rate_bytes, uint32_t* __restrict__ hist,
+                        uint32_t* __restrict__ unaligned_flag) {
+  __shared__ uint32_t local[kBucketBins];
+  for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) local[i] = 0u;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * (kBucketThreads * kBucketItems);
+  uint32_t misaligned = 0u;
+#pragma unroll
+  for (int k = 0; k < kBucketItems; ++k) {
+    const uint32_t i = base + k * kBucketThreads + threadIdx.x;
+    if (i < count) {
+      atomicAdd(&local[bucket_key(lengths[i], rate_bytes)], 1u);
+      misaligned |= static_cast<uint32_t>(offsets[i]) & 7u;
+    }
+  }
+  if (__any_sync(0xffffffffu, misaligned != 0u) && (threadIdx.x & 31) == 0) {
+    atomicOr(unaligned_flag, 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) {
+    if (local[i]) atomicAdd(&hist[i], local[i]);
+  }
+}
+
+// Exclusive scan of the 256 bins (one block): hist -> bin base; cursor <- 0.
+__global__ void __launch_bounds__(kBucketBins)
+bucket_scan_kernel(uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor) {
+  __shared__ uint32_t tmp[kBucketBins];
+  const int t = threadIdx.x;
+  const uint32_t mine = hist[t];
+  tmp[t] = mine;
+  __syncthreads();
+  for (int d = 1; d < kBucketBins; d <<= 1) {
+    const uint32_t add = t >= d ? tmp[t - d] : 0u;
+    __syncthreads();
+    tmp[t] += add;
+    __syncthreads();
+  }
+  hist[t] = tmp[t] - mine;
+  cursor[t] = 0u;
+}
+
+__global__ void __launch_bounds__(kBucketThreads)
+bucket_scatter_kernel(const uint64_t* __restrict__ lengths, uint32_t count,
+                      uint32_t rate_bytes, const uint32_t* __restrict__ bin_base,
+                      uint32_t* __restrict__ cursor, uint32_t* __restrict__ order) {
+  __shared__ uint32_t local[kBucketBins];   // per-block count, then block base
+  for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) local[i] = 0u;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * (kBucketThreads * kBucketItems);
+  uint32_t key[kBucketItems], rank[kBucketItems];
+#pragma unroll
+  for (int k = 0; k < kBucketItems; ++k) {
+    const uint32_t i = base + k * kBucketThreads + threadIdx.x;
+    if (i < count) {
+      key[k] = bucket_key(lengths[i], rate_bytes);
+      rank[k] = atomicAdd(&local[key[k]], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) {
+    const uint32_t n = local[i];
+    local[i] = n ? bin_base[i] + atomicAdd(&cursor[i], n) : 0u;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kBucketItems; ++k) {
+    const uint32_t i = base + k * kBucketThreads + threadIdx.x;
+    if (i < count) order[local[key[k]] + rank[k]] = i;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+alignment_check_kernel(const uint64_t* __restrict__ offsets, uint64_t count,
+                       uint32_t* __restrict__ unaligned_flag) {
+  uint32_t misaligned = 0u;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    misaligned |= static_cast<uint32_t>(offsets[i]) & 7u;
+  }
+  if (__any_sync(0xffffffffu, misaligned != 0u) && (threadIdx.x & 31) == 0) {
+    atomicOr(unaligned_flag, 1u);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Workloads.  splitmix64 is counter-based: output number n (1-based) of a
+// generator seeded with s is mix(s + n * gamma)
+// (proj/tools/sha3cli/workload.hpp:25-36), so any slice of the reference's
+// stream can be produced independently.
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t seed, uint64_t n) {
+  uint64_t z = seed + n * 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ void store_word_bytes(uint8_t* dst, uint64_t word, uint32_t nbytes) {
+  if (nbytes == 8u && (reinterpret_cast<uintptr_t>(dst) & 7u) == 0u) {
+    *reinterpret_cast<uint64_t*>(dst) = word;
+  } else {
+    for (uint32_t b = 0; b < nbytes; ++b) dst[b] = static_cast<uint8_t>(word >> (8u * b));
+  }
+}
+
+// generate_workload (proj/tools/sha3cli/workload.cpp:34-45): message i draws
+// ceil(size/8) consecutive words; surplus bytes of its last word are dropped.
+__global__ void __launch_bounds__(256)
+generate_workload_kernel(uint64_t stream_seed, uint64_t message_size, uint64_t words_per_msg,
+                         uint64_t first_message, uint64_t total_words, uint8_t* out) {
+  for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       w < total_words; w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = w / words_per_msg;
+    const uint64_t k = w - i * words_per_msg;
+    const uint64_t n = (first_message + i) * words_per_msg + k + 1u;
+    const uint64_t left = message_size - 8u * k;
+    store_word_bytes(out + i * message_size + 8u * k, splitmix_at(stream_seed, n),
+                     left < 8u ? static_cast<uint32_t>(left) : 8u);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+generate_lengths_kernel(uint64_t seed_len, uint64_t min_len, uint64_t span,
+                        uint64_t first_message, uint64_t count, uint64_t* lengths) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    lengths[i] = min_len + splitmix_at(seed_len, first_message + i + 1u) % span;
+  }
+}
+
+// One warp per message; lane k strides over the message's words.
+__global__ void __launch_bounds__(256)
+fill_messages_kernel(uint64_t seed, uint64_t first_message, uint64_t count,
+                     const uint64_t* __restrict__ offsets,
+                     const uint64_t* __restrict__ lengths, uint8_t* data) {
+  const uint64_t warps_per_grid = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint32_t lane = threadIdx.x & 31u;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       i < count; i += warps_per_grid) {
+    const uint64_t key = seed ^ ((first_message + i) * 0xd1342543de82ef95ull);
+    const uint64_t len = lengths[i];
+    uint8_t* dst = data + offsets[i];
+    const uint64_t words = (len + 7u) / 8u;
+    for (uint64_t k = lane; k < words; k += 32u) {
+      const uint64_t left = len - 8u * k;
+      store_word_bytes(dst + 8u * k, splitmix_at(key, k + 1u),
+                       left < 8u ? static_cast<uint32_t>(left) : 8u);
+    }
+  }
+}
+
+unsigned grid_for(uint64_t items, unsigned threads, unsigned cap = 148u * 32u) {
+  const uint64_t blocks = (items + threads - 1) / threads;
+  return static_cast<unsigned>(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
+}
+
+}  // namespace
+
+cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream) {
+  if (count == 0) return cudaSuccess;
+  const uint64_t blocks = (count + 127) / 128;
+  if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+  permute_kernel<<<static_cast<unsigned>(blocks), 128, 0, stream>>>(states, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,
+                                uint32_t count, uint32_t rate_bytes, uint32_t* order,
+                                uint32_t* scratch, uint32_t* unaligned_flag,
+                                cudaStream_t stream) {
+  if (count == 0) return cudaSuccess;
+  uint32_t* hist = scratch;
+  uint32_t* cursor = scratch + kBucketBins;
+  cudaError_t err = cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * kBucketScratchWords, stream);
+  if (err != cudaSuccess) return err;
+  const unsigned per_block = kBucketThreads * kBucketItems;
+  const unsigned blocks = (count + per_block - 1) / per_block;
+  bucket_histogram_kernel<<<blocks, kBucketThreads, 0, stream>>>(offsets, lengths, count,
+                                                                rate_bytes, hist,
+                                                                unaligned_flag);
+  bucket_scan_kernel<<<1, kBucketBins, 0, stream>>>(hist, cursor);
+  bucket_scatter_kernel<<<blocks, kBucketThreads, 0, stream>>>(lengths, count, rate_bytes,
+                                                              hist, cursor, order);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_alignment_check(const uint64_t* offsets, uint64_t count,
+                                   uint32_t* unaligned_flag, cudaStream_t stream) {
+  if (count == 0) return cudaSuccess;
+  alignment_check_kernel<<<grid_for(count, 256), 256, 0, stream>>>(offsets, count,
+                                                                  unaligned_flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_generate_workload(uint64_t stream_seed, uint64_t message_size,
+                                     uint64_t first_message, uint64_t count, uint8_t* out,
+                                     cudaStream_t stream) {
+  if (count == 0) return cudaSuccess;
+  const uint64_t wpm = (message_size + 7) / 8;
+  const uint64_t total_words = wpm * count;
+  generate_workload_kernel<<<grid_for(total_words, 256), 256, 0, stream>>>(
+      stream_seed, message_size, wpm, first_message, total_words, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_generate_lengths(uint64_t seed_len, uint64_t min_len, uint64_t max_len,
+                                    uint64_t first_message, uint64_t count,
+                                    uint64_t* lengths, cudaStream_t stream) {
+  if (count == 0) return cudaSuccess;
+  generate_lengths_kernel<<<grid_for(count, 256), 256, 0, stream>>>(
+      seed_len, min_len, max_len - min_len + 1, first_message, count, lengths);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_messages(uint64_t seed, uint64_t first_message, uint64_t count,
+                                 const uint64_t* offsets, const uint64_t* lengths,
+                                 uint8_t* data, cudaStream_t stream) {
+  if (count == 0) return cudaSuccess;
+  fill_messages_kernel<<<grid_for(count * 32, 256, 148u * 64u), 256, 0, stream>>>(
+      seed, first_message, count, offsets, lengths, data);
+  return cudaGetLastError();
+}
+
+}  // namespace b200sha3

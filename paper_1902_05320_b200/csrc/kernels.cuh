@@ -1,0 +1,100 @@
+// kernels.cuh -- kernel declarations shared by the translation units of
+// libb200sha3.so.  One message per thread unless stated otherwise.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace b200sha3 {
+
+// Arguments of the batch kernels (passed by value in the parameter bank).
+struct HashArgs {
+  const uint8_t* data;       // packed message bytes
+  const uint64_t* offsets;   // per-message byte offset, or nullptr: i * fixed_len
+  const uint64_t* lengths;   // per-message byte length, or nullptr: fixed_len
+  uint64_t fixed_len;
+  uint64_t count;
+  const uint32_t* order;     // processing order (bucketed), or nullptr: identity
+  const uint32_t* unaligned_flag;  // device word, nonzero if any message start is not
+                                   // 8-byte aligned; nullptr: use `aligned8`
+  uint8_t* digests;          // count * digest_bytes, message order
+  uint64_t digest_bytes;
+  uint32_t head;             // pad head byte: 0x06 / 0x1f
+  uint32_t last_mask;        // 0xff or the XOF partial-byte mask
+  uint32_t aligned8;         // host-known alignment of every message start
+};
+
+// FMA-pipe rotation presets (see keccak_f1600.cuh): bit i = rho rotation of
+// source lane i on the FMA pipe, bit 25 = theta rotl-1.
+constexpr uint32_t kRhoAll = 0x1fffffeu;    // all 24 rotating rho lanes
+constexpr uint32_t kRhoOdd = 0x0aaaaaau;    // 12 of them
+constexpr uint32_t kTheta = 0x2000000u;
+constexpr uint32_t kFlavour(int f) { return static_cast<uint32_t>(f) << 28; }
+constexpr int kFmaPresets = 9;
+constexpr uint32_t kFmaPreset[kFmaPresets] = {
+    0u,                                   // 0: ALU only (LOP3 + SHF)
+    kRhoAll | kTheta | kFlavour(1),       // 1: everything, flavour 1
+    kRhoAll | kFlavour(1),                // 2: all rho, flavour 1
+    kRhoOdd | kFlavour(1),                // 3: 12 rho, flavour 1
+    kRhoAll | kTheta | kFlavour(2),       // 4: everything, flavour 2
+    kRhoAll | kFlavour(2),                // 5: all rho, flavour 2
+    (kRhoOdd | 0x0000554u) | kFlavour(2), // 6: 17 rho, flavour 2
+    kRhoOdd | kFlavour(2),                // 7: 12 rho, flavour 2
+    0x0888888u | kFlavour(2),             // 8: 6 rho, flavour 2
+};
+
+struct LaunchPlan {
+  int rate_lanes;     // 9, 13, 17, 18, 21
+  int unroll;         // 1, 2, 4, 24 (availability depends on the kernel)
+  int fma_preset;     // 0..kFmaPresets-1
+  int block_threads;
+};
+
+// Generic kernel: any length, any alignment, multi-block absorb and squeeze.
+cudaError_t launch_hash_generic(const HashArgs& args, const LaunchPlan& plan,
+                                cudaStream_t stream);
+
+// Specialised kernel: equal-length, 16-byte aligned, single-block messages of
+// whole lanes with a digest of whole 32-bit words that fits one block.  Returns
+// cudaErrorNotSupported when no instantiation matches.
+cudaError_t launch_hash_oneblock(const HashArgs& args, const LaunchPlan& plan,
+                                 cudaStream_t stream);
+bool oneblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
+
+// Lane-split kernel (5 threads per state, warp shuffles); equal-length,
+// 8-byte aligned, single-block messages.
+cudaError_t launch_hash_lanesplit(const HashArgs& args, const LaunchPlan& plan,
+                                  cudaStream_t stream);
+bool lanesplit_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
+
+// Keccak-f[1600] on raw 200-byte states (test hook).
+cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream);
+
+// Bucketing by block count: writes a processing order (heaviest first) and sets
+// *unaligned_flag if any offset is not a multiple of 8.  `scratch` needs
+// kBucketScratchWords 32-bit words.
+constexpr int kBucketBins = 256;
+constexpr int kBucketScratchWords = 2 * kBucketBins + 8;
+cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,
+                                uint32_t count, uint32_t rate_bytes, uint32_t* order,
+                                uint32_t* scratch, uint32_t* unaligned_flag,
+                                cudaStream_t stream);
+// Alignment check only (no ordering).
+cudaError_t launch_alignment_check(const uint64_t* offsets, uint64_t count,
+                                   uint32_t* unaligned_flag, cudaStream_t stream);
+
+// Synthetic workloads.
+cudaError_t launch_generate_workload(uint64_t stream_seed, uint64_t message_size,
+                                     uint64_t first_message, uint64_t count, uint8_t* out,
+                                     cudaStream_t stream);
+cudaError_t launch_generate_lengths(uint64_t seed_len, uint64_t min_len, uint64_t max_len,
+                                    uint64_t first_message, uint64_t count,
+                                    uint64_t* lengths, cudaStream_t stream);
+cudaError_t launch_fill_messages(uint64_t seed, uint64_t first_message, uint64_t count,
+                                 const uint64_t* offsets, const uint64_t* lengths,
+                                 uint8_t* data, cudaStream_t stream);
+
+// Pipe microbenchmark; see b200sha3_probe_pipe.
+cudaError_t run_pipe_probe(int mix, double* instr_per_s, double* sm_hz, cudaStream_t stream);
+
+}  // namespace b200sha3

@@ -1,0 +1,211 @@
+// sponge.cuh -- per-thread sponge: pad / absorb / squeeze around keccak_f1600.
+//
+// Replaces, for one message per thread, the reference's SpongeHasher
+// (proj/core/src/sponge.cpp:71-149) as driven by hash_into
+// (proj/core/src/batch.cpp:15-25):
+//   update  (sponge.cpp:81-111)  -> absorb_lanes_aligned / absorb_words_unaligned
+//   finish  (sponge.cpp:113-129) -> absorb_tail_* (pad head byte at `rem`,
+//                                   0x80 into the last rate byte)
+//   squeeze (sponge.cpp:131-143) -> emit_block
+//   XOF bit mask (batch.cpp:22-24) -> hash_message epilogue
+//
+// RL is the rate in 64-bit lanes (9, 13, 17, 18 or 21; sha3.cpp:13-20).  All
+// state indices are compile-time; runtime lengths are handled with predicated,
+// fully unrolled loops so the state stays in registers.
+#pragma once
+#include <cstdint>
+
+#include "keccak_f1600.cuh"
+
+namespace b200sha3 {
+
+__device__ __forceinline__ uint2 ld_u2(const uint2* p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ld_u32(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ld_u8(const uint8_t* p) { return __ldg(p); }
+
+// XOR `lanes` (<= RL) 64-bit words from the 8-byte aligned pointer p into the state.
+template <int RL>
+__device__ __forceinline__ void absorb_lanes_aligned(State& a, const uint8_t* p,
+                                                     uint32_t lanes) {
+  const uint2* q = reinterpret_cast<const uint2*>(p);
+#pragma unroll
+  for (int i = 0; i < RL; ++i) {
+    if (static_cast<uint32_t>(i) < lanes) {
+      const uint2 v = ld_u2(q + i);
+      a.lo[i] ^= v.x;
+      a.hi[i] ^= v.y;
+    }
+  }
+}
+
+// XOR `words` (<= 2*RL) 32-bit words from the arbitrarily aligned pointer p into
+// the state: aligned 4-byte loads re-assembled with PRMT.  Only aligned words
+// that contain at least one byte of [p, p + 4*words) are touched.
+template <int RL>
+__device__ __forceinline__ void absorb_words_unaligned(State& a, const uint8_t* p,
+                                                       uint32_t words) {
+  const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p)) & 3u;
+  const uint32_t* q = reinterpret_cast<const uint32_t*>(p - sh);
+  const uint32_t sel = 0x3210u + 0x1111u * sh;
+  const uint32_t nload = words ? words + (sh ? 1u : 0u) : 0u;
+  uint32_t prev = nload ? ld_u32(q) : 0u;
+#pragma unroll
+  for (int j = 0; j < 2 * RL; ++j) {
+    const uint32_t next = (static_cast<uint32_t>(j) + 1u < nload) ? ld_u32(q + j + 1) : 0u;
+    const uint32_t w = (static_cast<uint32_t>(j) < words) ? __byte_perm(prev, next, sel) : 0u;
+    if (j & 1) {
+      a.hi[j >> 1] ^= w;
+    } else {
+      a.lo[j >> 1] ^= w;
+    }
+    prev = next;
+  }
+}
+
+// Final (partial) block: `rem` < 8*RL message bytes at p, then the pad.
+//   head = suffix | 1 << suffix_bits  (0x06 / 0x1f), XORed at byte `rem`;
+//   0x80 XORed at byte 8*RL - 1 (the same byte when rem == 8*RL - 1).
+template <int RL>
+__device__ __forceinline__ void absorb_tail(State& a, const uint8_t* p, uint32_t rem,
+                                            uint32_t head, bool aligned8) {
+  if (aligned8) {
+    const uint32_t fl = rem >> 3, rb = rem & 7u;
+    absorb_lanes_aligned<RL>(a, p, fl);
+    const uint8_t* tp = p + 8u * fl;
+    uint32_t tlo = 0u, thi = 0u;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (static_cast<uint32_t>(b) < rb) tlo |= ld_u8(tp + b) << (8 * b);
+    }
+#pragma unroll
+    for (int b = 4; b < 7; ++b) {
+      if (static_cast<uint32_t>(b) < rb) thi |= ld_u8(tp + b) << (8 * (b - 4));
+    }
+    if (rb < 4u) {
+      tlo |= head << (8u * rb);
+    } else {
+      thi |= head << (8u * (rb - 4u));
+    }
+#pragma unroll
+    for (int i = 0; i < RL; ++i) {
+      if (static_cast<uint32_t>(i) == fl) {
+        a.lo[i] ^= tlo;
+        a.hi[i] ^= thi;
+      }
+    }
+  } else {
+    const uint32_t fw = rem >> 2, rb = rem & 3u;
+    absorb_words_unaligned<RL>(a, p, fw);
+    const uint8_t* tp = p + 4u * fw;
+    uint32_t t = head << (8u * rb);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      if (static_cast<uint32_t>(b) < rb) t |= ld_u8(tp + b) << (8 * b);
+    }
+#pragma unroll
+    for (int j = 0; j < 2 * RL; ++j) {
+      if (static_cast<uint32_t>(j) == fw) {
+        if (j & 1) {
+          a.hi[j >> 1] ^= t;
+        } else {
+          a.lo[j >> 1] ^= t;
+        }
+      }
+    }
+  }
+  a.hi[RL - 1] ^= 0x80000000u;
+}
+
+__device__ __forceinline__ uint32_t state_word(const State& a, int j) {
+  return (j & 1) ? a.hi[j >> 1] : a.lo[j >> 1];
+}
+
+// Writes the first n (<= 8*RL) bytes of the rate part, little-endian, to o.
+// 16-byte stores when o and n allow, else 4-byte stores plus a byte tail, else
+// byte stores.
+template <int RL>
+__device__ __forceinline__ void emit_block(const State& a, uint8_t* o, uint32_t n) {
+  const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(o));
+  if (((mis | n) & 15u) == 0u) {
+#pragma unroll
+    for (int k = 0; k < (2 * RL + 3) / 4; ++k) {
+      if (16u * k + 16u <= n) {
+        // k indexes whole uint4 groups; lanes 2k, 2k+1 always exist for 16k+16 <= 8*RL
+        uint4 v;
+        v.x = state_word(a, (4 * k + 0 < 2 * RL) ? 4 * k + 0 : 0);
+        v.y = state_word(a, (4 * k + 1 < 2 * RL) ? 4 * k + 1 : 0);
+        v.z = state_word(a, (4 * k + 2 < 2 * RL) ? 4 * k + 2 : 0);
+        v.w = state_word(a, (4 * k + 3 < 2 * RL) ? 4 * k + 3 : 0);
+        *reinterpret_cast<uint4*>(o + 16 * k) = v;
+      }
+    }
+  } else if ((mis & 3u) == 0u) {
+#pragma unroll
+    for (int j = 0; j < 2 * RL; ++j) {
+      const uint32_t w = state_word(a, j);
+      if (4u * j + 4u <= n) {
+        *reinterpret_cast<uint32_t*>(o + 4 * j) = w;
+      } else if (4u * j < n) {
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          if (4u * j + b < n) o[4 * j + b] = static_cast<uint8_t>(w >> (8 * b));
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 2 * RL; ++j) {
+      const uint32_t w = state_word(a, j);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (4u * j + b < n) o[4 * j + b] = static_cast<uint8_t>(w >> (8 * b));
+      }
+    }
+  }
+}
+
+// One whole message: the a4 -> a5 -> a6 -> a7 sequence of SURVEY.md section 8(a).
+//   p/len        message bytes (any alignment unless aligned8 says otherwise)
+//   out/out_len  digest slot, out_len >= 1
+//   head         0x06 (SHA-3) or 0x1f (SHAKE)
+//   last_mask    0xff, or (1 << bits%8) - 1 for an XOF length that is not a
+//                multiple of 8 (batch.cpp:22-24)
+// The permutation is instantiated once: absorb blocks and squeeze blocks share
+// one loop.
+template <int RL, int UNROLL, uint32_t FMA_MASK>
+__device__ __forceinline__ void hash_message(const uint8_t* p, uint64_t len, uint8_t* out,
+                                             uint64_t out_len, uint32_t head,
+                                             uint32_t last_mask, bool aligned8) {
+  constexpr uint32_t R = 8u * RL;
+  State a;
+  state_zero(a);
+  const uint64_t nfull = len / R;
+  const uint32_t rem = static_cast<uint32_t>(len - nfull * R);
+  const uint64_t iters = nfull + 1u + (out_len - 1u) / R;
+  uint8_t* o = out;
+  uint64_t left = out_len;
+  for (uint64_t it = 0; it < iters; ++it) {
+    if (it < nfull) {
+      if (aligned8) {
+        absorb_lanes_aligned<RL>(a, p, RL);
+      } else {
+        absorb_words_unaligned<RL>(a, p, 2 * RL);
+      }
+      p += R;
+    } else if (it == nfull) {
+      absorb_tail<RL>(a, p, rem, head, aligned8);
+    }
+    keccak_f1600<UNROLL, FMA_MASK>(a);
+    if (it >= nfull) {
+      const uint32_t n = left < R ? static_cast<uint32_t>(left) : R;
+      emit_block<RL>(a, o, n);
+      o += n;
+      left -= n;
+    }
+  }
+  if (last_mask != 0xffu) {
+    out[out_len - 1u] &= static_cast<uint8_t>(last_mask);
+  }
+}
+
+}  // namespace b200sha3

@@ -1,0 +1,326 @@
+"""Parity tests proper: the CUDA path, called through the C ABI, against the
+CPU oracle and the committed golden vectors -- bit-exact (bytes in, bytes out;
+there is no floating point on this path)."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from batches import materialize, ref_batch_cases
+from conftest import all_kat_files, load_kat_file, xof_bits_for
+
+pytestmark = pytest.mark.gpu
+
+
+def pack(messages, align=1, lead=0):
+    """Packs messages into one buffer with every start at `lead` mod `align`."""
+    lengths = np.array([len(m) for m in messages], dtype=np.uint64)
+    offsets = np.zeros(len(messages), dtype=np.uint64)
+    pos = lead
+    chunks = [b"\xEE" * lead]
+    for i, m in enumerate(messages):
+        pad = (-(pos - lead)) % align
+        chunks.append(b"\xEE" * pad)
+        pos += pad
+        offsets[i] = pos
+        chunks.append(bytes(m))
+        pos += len(m)
+    data = np.frombuffer(b"".join(chunks) + b"\xEE", dtype=np.uint8).copy()
+    return data, offsets, lengths
+
+
+def to_device(*arrays):
+    import torch
+    out = []
+    for a in arrays:
+        t = torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).cuda()
+        out.append(t)
+    return out
+
+
+def device_digests(engine, algorithm, messages, bits=0, align=1, lead=0, **kw):
+    import torch
+    data, offsets, lengths = pack(messages, align, lead)
+    d, o, l = to_device(data, offsets, lengths)
+    out = engine.hash_batch(algorithm, d, o, l, xof_output_bits=bits, **kw)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def test_native_library_is_loaded(engine):
+    from paper_1902_05320_b200 import library_path
+    maps = open("/proc/self/maps").read()
+    assert str(library_path()) in maps
+
+
+def test_permutation_kat(engine, inline_kats, oracle):
+    """Keccak-f[1600](0) (test_keccak.cpp:456-466) and random states vs the oracle."""
+    import torch
+    rng = np.random.default_rng(11)
+    states = rng.integers(0, 2**63, (1000, 25), dtype=np.uint64)
+    states[0] = 0
+    t = torch.from_numpy(states.view(np.int64).copy()).cuda()
+    engine.permute_states(t)
+    got = t.cpu().numpy().view(np.uint64)
+    assert got[0].tobytes().hex() == inline_kats["keccak_f1600_zero_state"]["state"]
+    for i in range(0, 1000, 37):
+        assert (got[i] == oracle.permute(states[i])).all()
+
+
+@pytest.mark.parametrize("path", all_kat_files(), ids=lambda p: p.stem)
+def test_reference_vectors_device_path(engine, path):
+    """All 892 .rsp vectors, each file as ONE batch (every length 0..R+16 and
+    the long messages side by side in a warp), packed at odd offsets."""
+    algorithm, out_bits, vectors = load_kat_file(path)
+    bits = xof_bits_for(algorithm, out_bits)
+    msgs = [m for m, _ in vectors]
+    for align, lead in ((1, 0), (8, 0), (1, 3)):
+        got = device_digests(engine, algorithm, msgs, bits, align, lead)
+        for row, (_, md) in zip(got, vectors):
+            assert row.tobytes() == md
+
+
+@pytest.mark.parametrize("path", all_kat_files(), ids=lambda p: p.stem)
+def test_reference_vectors_host_path(engine, path):
+    """Same vectors through the host-buffer entry (the hash_batch drop-in)."""
+    algorithm, out_bits, vectors = load_kat_file(path)
+    got = engine.hash_messages(algorithm, [m for m, _ in vectors], xof_bits_for(algorithm, out_bits))
+    assert got == [md for _, md in vectors]
+
+
+def test_inline_kats(engine, inline_kats):
+    for key, msg in (("empty_message", b""), ("msg_1600_bits_a3", b"\xa3" * 200)):
+        for algorithm in range(6):
+            bits = inline_kats[key]["xof_bits"][algorithm]
+            got = engine.hash_messages(algorithm, [msg], bits)[0]
+            assert got.hex() == inline_kats[key]["digests"][algorithm]
+    assert engine.hash_messages("sha3_256", [b"abc"])[0].hex() == inline_kats["sha3_256_abc"]["digest"]
+
+
+def test_hundred_copies_of_one_message(engine, oracle):
+    """test_batch.cpp:102-111 (the paper's 10-byte example)."""
+    msgs = [bytes([0x42] * 10)] * 100
+    got = engine.hash_messages("sha3_256", msgs)
+    assert got == [oracle.hash_one(1, msgs[0])] * 100
+
+
+def test_variable_lengths_example(engine, oracle):
+    """test_batch.cpp:169-176."""
+    msgs = [b"", bytes([1] * 1000), bytes([5]), bytes([2] * 137)]
+    assert engine.hash_messages("sha3_256", msgs) == [oracle.hash_one(1, m) for m in msgs]
+
+
+def test_xof_328_bits_example(engine, oracle):
+    """test_batch.cpp:150-160."""
+    msgs = [bytes([1, 2, 3]), b"", bytes([9, 9, 9, 9])]
+    got = engine.hash_messages("shake128", msgs, 328)
+    assert [len(g) for g in got] == [41, 41, 41]
+    assert got == [oracle.hash_one(4, m, 328) for m in msgs]
+
+
+@pytest.mark.parametrize("case", ref_batch_cases(), ids=lambda c: c["name"])
+def test_reference_batch_fixtures(engine, oracle, case):
+    """Outputs of the compiled reference (tests/golden/ref_batches.json):
+    multi-block squeeze, odd XOF bit counts, long and ragged batches -- device
+    path (bucketed and not) and host path."""
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_BUCKETING
+    msgs, _ = materialize(oracle, case["kind"], case["seed"], case["count"], case["max_len"])
+    a, bits = case["algorithm"], case["xof_bits"]
+    for got in (device_digests(engine, a, msgs, bits),
+                device_digests(Engine(flags=FLAG_NO_BUCKETING), a, msgs, bits, align=8),
+                np.stack([np.frombuffer(d, np.uint8) for d in engine.hash_messages(a, msgs, bits)])):
+        assert got.shape == (case["count"], case["digest_bytes"])
+        assert got[0].tobytes().hex() == case["first"]
+        assert got[-1].tobytes().hex() == case["last"]
+        assert hashlib.sha3_256(got.tobytes()).hexdigest() == case["checksum_sha3_256"]
+
+
+@pytest.mark.parametrize("algorithm", range(6))
+def test_block_boundary_lengths_vs_oracle(engine, oracle, algorithm):
+    """Every length around the block boundaries (R-1: 0x06|0x80 in one byte; R:
+    pad-only extra block), several alignments, several output lengths."""
+    rate = oracle.rate_bytes(algorithm)
+    rng = np.random.default_rng(100 + algorithm)
+    lens = sorted(set(list(range(0, 20)) + list(range(rate - 10, rate + 10)) +
+                      list(range(2 * rate - 3, 2 * rate + 3)) + [3 * rate, 7 * rate - 1, 5000]))
+    msgs = [rng.integers(0, 256, n, dtype=np.uint8).tobytes() for n in lens]
+    for bits in ([0] if algorithm < 4 else [8, 12, 8 * rate, 8 * rate + 8, 3 * 8 * rate + 5]):
+        expect = [oracle.hash_one(algorithm, m, bits) for m in msgs]
+        for align, lead in ((1, 0), (1, 5), (4, 0), (8, 0), (16, 0)):
+            got = device_digests(engine, algorithm, msgs, bits, align, lead)
+            assert [g.tobytes() for g in got] == expect, (bits, align, lead)
+
+
+@pytest.mark.parametrize("algorithm,msg_len", [(0, 32), (0, 64), (0, 1024), (1, 64), (1, 136), (1, 200),
+                                               (2, 32), (2, 128), (2, 512), (3, 72), (3, 1024), (3, 7),
+                                               (4, 64), (5, 64), (1, 10), (1, 0)])
+def test_fixed_length_batches(engine, oracle, algorithm, msg_len):
+    """cfg2/cfg3-shaped batches at oracle-friendly sizes, device and host entries,
+    on the reference's own synthetic stream."""
+    import torch
+    count = 3000
+    total = max(count * msg_len, 1)
+    bits = 0 if algorithm < 4 else 1024
+    if msg_len:
+        host = oracle.generate_workload(total, msg_len, seed=1)
+        dev = engine.generate_workload(total, msg_len, seed=1)
+        assert (dev.cpu().numpy() == host).all()      # device generator == workload.cpp
+    else:
+        host = np.zeros(1, np.uint8)
+        dev = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    expect = oracle.hash_batch(algorithm, host, fixed_len=msg_len, count=count, xof_bits=bits, workers=4)
+    got = engine.hash_fixed(algorithm, dev, msg_len, count, bits)
+    torch.cuda.synchronize()
+    assert (got.cpu().numpy() == expect).all()
+    assert (engine.hash_fixed(algorithm, host, msg_len, count, bits) == expect).all()
+
+
+def test_every_kernel_variant_agrees(engine, oracle):
+    """The tuning matrix (unroll x FMA-offload presets, one-block and generic)
+    must be invisible in the digests."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import KERNEL_GENERIC, KERNEL_ONEBLOCK
+    count = 5000
+    host = oracle.generate_workload(count * 64, 64, seed=9)
+    dev = torch.from_numpy(host).cuda()
+    expect = oracle.hash_batch(1, host, fixed_len=64, count=count, workers=4)
+    for unroll in (2, 4, 24):
+        for preset in range(9):
+            e = Engine(kernel=KERNEL_ONEBLOCK, unroll=unroll, fma_preset=preset)
+            got = e.hash_fixed("sha3_256", dev, 64, count)
+            assert (got.cpu().numpy() == expect).all(), (unroll, preset)
+    for preset in (0, 5):
+        for threads in (64, 128, 256):
+            e = Engine(kernel=KERNEL_GENERIC, fma_preset=preset, block_threads=threads)
+            assert (e.hash_fixed("sha3_256", dev, 64, count).cpu().numpy() == expect).all()
+    # SHAKE256 shares rate 17 / 32-byte output with SHA3-256 but not the pad byte
+    expect_xof = oracle.hash_batch(5, host, fixed_len=64, count=count, xof_bits=256, workers=4)
+    got = Engine(kernel=KERNEL_ONEBLOCK).hash_fixed("shake256", dev, 64, count, 256)
+    assert (got.cpu().numpy() == expect_xof).all()
+
+
+def test_bucket_order_is_a_sorted_permutation(engine):
+    """Device bucketing: every index exactly once, block counts non-increasing
+    up to the bin width."""
+    import torch
+    lengths = engine.generate_lengths(200_000, 1, 16384, seed_len=2)
+    order = engine.bucket_order("sha3_256", lengths).cpu().numpy().astype(np.int64)
+    assert np.array_equal(np.sort(order), np.arange(200_000))
+    blocks = (lengths.cpu().numpy() // 136 + 1)[order]
+    assert blocks[0] == blocks.max() and blocks[-1] == blocks.min()
+    assert (np.diff(blocks) <= 0).all()      # below 128 blocks every bin is one block count
+    torch.cuda.synchronize()
+
+
+def test_variable_length_workload_vs_oracle(engine, oracle):
+    """cfg4-shaped batch (lengths 1..16 KiB from the device generator) on a
+    subsample the oracle finishes quickly; bucketed == unbucketed == oracle."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_BUCKETING, splitmix64_at
+    count = 4096
+    lengths = engine.generate_lengths(count, 1, 16384, seed_len=2)
+    host_len = lengths.cpu().numpy().astype(np.uint64)
+    expect_len = 1 + splitmix64_at(np.uint64(2), np.arange(1, count + 1, dtype=np.uint64)) % np.uint64(16384)
+    assert (host_len == expect_len).all()
+    padded = (lengths + 7) // 8 * 8
+    offsets = torch.cumsum(padded, 0) - padded
+    data = torch.zeros(int(padded.sum().item()) + 16, dtype=torch.uint8, device="cuda")
+    engine.fill_messages(data, offsets, lengths, seed=1)
+    got = engine.hash_batch("sha3_256", data, offsets, lengths)
+    got2 = Engine(flags=FLAG_NO_BUCKETING).hash_batch("sha3_256", data, offsets, lengths)
+    torch.cuda.synchronize()
+    expect = oracle.hash_batch(1, data.cpu().numpy(), offsets.cpu().numpy().astype(np.uint64), host_len,
+                               workers=8)
+    assert (got.cpu().numpy() == expect).all()
+    assert (got2.cpu().numpy() == expect).all()
+    # message content generator: word k of message i = splitmix(seed ^ i*C, k+1)
+    i = 5
+    key = np.uint64(1) ^ np.uint64((i * 0xd1342543de82ef95) & (2**64 - 1))
+    n = int(host_len[i])
+    words = splitmix64_at(key, np.arange(1, (n + 7) // 8 + 1, dtype=np.uint64)).view(np.uint8)[:n]
+    off = int(offsets[i].item())
+    assert (data[off:off + n].cpu().numpy() == words).all()
+
+
+def test_full_size_properties_cfg1(engine, oracle):
+    """cfg1 at full size (2^20 x 64 B): sampled digests vs the oracle, a checksum
+    of all digests vs the oracle's, sharding invariance, and determinism."""
+    import torch
+    count, total = 1 << 20, 1 << 26
+    dev = engine.generate_workload(total, 64, seed=1)
+    got = engine.hash_fixed("sha3_256", dev, 64, count)
+    again = engine.hash_fixed("sha3_256", dev, 64, count)
+    assert torch.equal(got, again)
+    host = dev.cpu().numpy()
+    expect = oracle.hash_batch(1, host, fixed_len=64, count=count, workers=8)
+    g = got.cpu().numpy()
+    assert hashlib.sha3_256(g.tobytes()).hexdigest() == hashlib.sha3_256(expect.tobytes()).hexdigest()
+    # contiguous shards generated independently (as ranks do) give the same digests
+    for first, n in ((0, 1000), (123_456, 4096), (count - 77, 77)):
+        shard = engine.generate_workload(total, 64, seed=1, first_message=first, count=n)
+        part = engine.hash_fixed("sha3_256", shard, 64, n)
+        assert torch.equal(part, got[first:first + n])
+
+
+def test_large_batch_roundtrip_properties(engine, oracle):
+    """2^24 x 64 B (1 GiB): no oracle pass over everything -- sample 4096
+    messages against the oracle and check the one-block and generic kernels agree
+    on all 2^24 digests."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import KERNEL_GENERIC
+    count = 1 << 24
+    dev = engine.generate_workload(count * 64, 64, seed=3)
+    fast = engine.hash_fixed("sha3_256", dev, 64, count)
+    slow = Engine(kernel=KERNEL_GENERIC).hash_fixed("sha3_256", dev, 64, count)
+    assert torch.equal(fast, slow)
+    idx = torch.randint(0, count, (4096,), generator=torch.Generator().manual_seed(5))
+    msgs = dev.view(count, 64)[idx.cuda()].cpu().numpy()
+    expect = oracle.hash_batch(1, msgs, fixed_len=64, count=4096, workers=8)
+    assert (fast[idx.cuda()].cpu().numpy() == expect).all()
+
+
+def test_host_entry_pipelined_equals_single_shot(engine, oracle):
+    """Host-buffer entry with and without the chunked copy/compute pipeline
+    (3 x 64 MiB slots), pageable and pinned memory."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_PIPELINE
+    count = 3_000_001               # ~183 MiB in: several chunks, ragged tail
+    host = oracle.generate_workload(count * 64, 64, seed=4)
+    a = engine.hash_fixed("sha3_256", host, 64, count)
+    b = Engine(flags=FLAG_NO_PIPELINE).hash_fixed("sha3_256", host, 64, count)
+    assert (a == b).all()
+    pinned = torch.from_numpy(host).pin_memory()
+    out = torch.empty((count, 32), dtype=torch.uint8).pin_memory()
+    engine.hash_fixed_ptr("sha3_256", pinned.data_ptr(), 64, count, out.data_ptr())
+    assert (out.numpy() == a).all()
+    sample = np.arange(0, count, 9973)
+    expect = oracle.hash_batch(1, host.reshape(count, 64)[sample], fixed_len=64, count=len(sample))
+    assert (a[sample] == expect).all()
+
+
+def test_reentrant_from_multiple_callers(engine, oracle):
+    """test_batch.cpp:178-196: three threads, each with its own batch call."""
+    import threading
+    rng = oracle.test_rng(54)
+    msgs = [rng.random_bytes(rng.below(31)) for _ in range(200)]
+    expect = [oracle.hash_one(1, m) for m in msgs]
+    ok = [False] * 3
+
+    def run(t):
+        from paper_1902_05320_b200 import Engine
+        ok[t] = Engine().hash_messages("sha3_256", msgs) == expect
+
+    threads = [threading.Thread(target=run, args=(t,)) for t in range(3)]
+    [t.start() for t in threads]
+    [t.join() for t in threads]
+    assert all(ok)
+
+
+def test_xof_without_length_rejected_on_gpu_box_too(engine):
+    with pytest.raises(ValueError):
+        engine.hash_messages("shake256", [b"\x01"], 0)
