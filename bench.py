@@ -1,0 +1,360 @@
+#!/usr/bin/env python3
+"""bench.py -- the headline benchmark of the batch SHA-3 path.
+
+    python bench.py --gpus N --steps K --warmup W            (N=1 directly,
+    python -m torch.distributed.run ... bench.py --gpus N    one rank per GPU for N>1)
+    python bench.py --impl reference ...                     (the reference's CPU path)
+
+Workload (BASELINE.json configs[4], the one the metric is quoted on): SHA3-256
+over 2^28 x 64-byte messages of the reference's synthetic stream
+(proj/tools/sha3cli/workload.cpp:16-47, seed 1), sharded over the N ranks by
+contiguous message ranges; no collective on the data path.  One "step" = one
+pass of the hot path over the rank's shard, input already resident in HBM,
+digests left in HBM.  The total is fixed, so the run is a strong-scaling run.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+ALGORITHM = "sha3_256"
+MSG_LEN = 64
+DIGEST_BYTES = 32
+INSTR_PER_PERMUTATION = 4320        # 122 LOP3 + 58 SHF per round x 24
+METRIC = "SHA3-256 hashes/s on 64-B msg batches"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--log2-messages", type=int, default=28, help="total messages across all GPUs")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = min(steps, 5)")
+    ap.add_argument("--cpu-log2-messages", type=int, default=22, help="CPU baseline sample size")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-probe", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------
+# clocks: sample nvidia-smi while the timed region runs (B200_PROFILING.md)
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu_index = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu_index}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._pump, daemon=True)
+        self.thread.start()
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        busy = [c for c, p in zip(sm, power) if p > 0.5 * max(power)] if power else sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    path = ROOT / "MEASURED_PEAKS.json"
+    if path.exists():
+        try:
+            d = json.loads(path.read_text())
+            return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "measured (MEASURED_PEAKS.json)"
+        except (ValueError, KeyError):
+            pass
+    return 6650.0, 1965.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic_per_launch(count_per_launch: int):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, scaled
+    to this launch's message count (traffic is linear in messages); None if not captured."""
+    path = ROOT / "profiles" / "roofline_traffic.json"
+    if not path.exists():
+        return None
+    try:
+        d = json.loads(path.read_text())
+        return d["dram_bytes_per_message"] * count_per_launch
+    except (ValueError, KeyError):
+        return None
+
+
+# --------------------------------------------------------------------------
+def cpu_baseline(log2_messages: int, steps: int, warmup: int):
+    """The reference's own hash_batch (oracle/_ref, compiled from /root/reference) or,
+    where that library does not exist, the C restatement -- on the host cores, on a bounded
+    sample of the SAME workload stream.  Median of `steps` runs after `warmup`."""
+    from oracle.binding import Oracle, Reference
+    count = 1 << log2_messages
+    total_bytes = (1 << 28) * MSG_LEN            # the stream of the full workload; we take its head
+    oracle = Oracle()
+    # head of the full-size stream: same seed derivation as the GPU arm (seed ^ total*gamma,
+    # workload.cpp:34); word n of the stream is splitmix64 output number n
+    import numpy as np
+    data = np.zeros(count * MSG_LEN, dtype=np.uint8)
+    state_seed = (1 ^ (total_bytes * 0x9e3779b97f4a7c15)) & (2**64 - 1)
+    from paper_1902_05320_b200.engine import splitmix64_at
+    words = splitmix64_at(np.uint64(state_seed), np.arange(1, count * 8 + 1, dtype=np.uint64))
+    data[:] = words.view(np.uint8)
+    cores = os.cpu_count() or 1
+    if Reference.available():
+        ref = Reference()
+        cores = ref.hardware_workers()
+        batch = Reference.Batch(ref, 1, data, MSG_LEN, count)
+        times = [batch.run(parallel=True, workers=0) for _ in range(warmup + steps)][warmup:]
+        seq_count = min(count, 1 << 20)
+        seq_batch = Reference.Batch(ref, 1, data[:seq_count * MSG_LEN], MSG_LEN, seq_count)
+        seq = [seq_batch.run(parallel=False) for _ in range(3)]
+        batch.close()
+        seq_batch.close()
+        kind = "reference"
+        seq_rate = seq_count / statistics.median(seq)
+    else:
+        t = []
+        for _ in range(warmup + steps):
+            t0 = time.perf_counter()
+            oracle.hash_batch(1, data, fixed_len=MSG_LEN, count=count, workers=cores)
+            t.append(time.perf_counter() - t0)
+        times = t[warmup:]
+        kind = "port"
+        t0 = time.perf_counter()
+        oracle.hash_batch(1, data, fixed_len=MSG_LEN, count=min(count, 1 << 20), workers=1)
+        seq_rate = min(count, 1 << 20) / (time.perf_counter() - t0)
+    med = statistics.median(times)
+    return {"value": count / med, "unit": "hashes/s", "cores": cores, "kind": kind,
+            "sample": f"first 2^{log2_messages} messages of the same stream, hash_batch "
+                      f"Backend::parallel workers={cores}, median of {steps} runs after {warmup} warm-up",
+            "ms_per_run": med * 1e3, "sequential_1core_hashes_per_s": seq_rate}, med
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    base, med = cpu_baseline(args.cpu_log2_messages, args.steps, args.warmup)
+    count = 1 << args.cpu_log2_messages
+    line = {
+        "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "hashes/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": med * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (reference generate_workload stream, seed 1)",
+        "config": {"workload": f"SHA3-256 over 2^{args.log2_messages} x 64-byte messages (BASELINE.json "
+                               f"configs[4]); each step a bounded sample of 2^{args.cpu_log2_messages} "
+                               "messages on the host cores", "messages_per_step": count,
+                   "message_bytes": MSG_LEN},
+        "gb_per_s_hashed": base["value"] * MSG_LEN / 1e9,
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "hashes/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1902_05320_b200 import Engine
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torch.distributed.run")
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    total = 1 << args.log2_messages
+    total_bytes = total * MSG_LEN
+    # contiguous message range per rank (plan_partition analogue, batch.cpp:46-62)
+    first = total * rank // world
+    count = total * (rank + 1) // world - first
+
+    engine = Engine(device=local_rank)
+    data = engine.generate_workload(total_bytes, MSG_LEN, seed=1, first_message=first, count=count)
+    digests = torch.empty((count, DIGEST_BYTES), dtype=torch.uint8, device="cuda")
+
+    for _ in range(args.warmup):
+        engine.hash_fixed(ALGORITHM, data, MSG_LEN, count, out=digests)
+    sampler = ClockSampler(local_rank)
+    if rank == 0:
+        sampler.start()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches_before = engine.total_kernel_launches
+    barrier()
+    start.record()
+    for _ in range(args.steps):
+        engine.hash_fixed(ALGORITHM, data, MSG_LEN, count, out=digests)
+    stop.record()
+    barrier()
+    clocks = sampler.stop() if rank == 0 else None
+    seconds = max_over_ranks(start.elapsed_time(stop) * 1e-3)
+    launches = engine.total_kernel_launches - launches_before
+    value = total * args.steps / seconds
+
+    # checksum of this rank's digests: proves the timed kernels did the work (and lets a
+    # reader compare runs at different N: the XOR over ranks is N-independent)
+    fold = digests.view(torch.int64).view(-1)
+    checksum = int(torch.bitwise_xor(fold[0::2], fold[1::2]).sum().item()) & (2**64 - 1)
+    if world > 1:
+        t = torch.tensor([checksum >> 1], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        checksum = int(t.item())
+
+    # ---- end to end through the host-buffer C entry (pinned host memory) -----------
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty(count * MSG_LEN, dtype=torch.uint8).pin_memory()
+        host_out = torch.empty(count * DIGEST_BYTES, dtype=torch.uint8).pin_memory()
+        host_in.copy_(data)
+        torch.cuda.synchronize()
+        e2e_steps = args.e2e_steps or min(args.steps, 5)
+        engine.hash_fixed_ptr(ALGORITHM, host_in.data_ptr(), MSG_LEN, count, host_out.data_ptr())
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            engine.hash_fixed_ptr(ALGORITHM, host_in.data_ptr(), MSG_LEN, count, host_out.data_ptr())
+        torch.cuda.synchronize()
+        e2e_seconds = max_over_ranks(time.perf_counter() - t0)
+        same = bool(torch.equal(host_out.view(count, DIGEST_BYTES)[:4096], digests[:4096].cpu()))
+        e2e = {"value": total * e2e_steps / e2e_seconds, "unit": "hashes/s",
+               "h2d_bytes_per_step": total * MSG_LEN, "d2h_bytes_per_step": total * DIGEST_BYTES,
+               "steps": e2e_steps, "ms_per_step": e2e_seconds / e2e_steps * 1e3,
+               "digests_match_device_path": same,
+               "note": "b200sha3_hash_fixed on pinned host buffers: chunked H2D / kernel / D2H "
+                       "pipeline inside the call; wall clock, max over ranks"}
+        del host_in, host_out
+
+    if rank == 0:
+        hbm_peak, sm_max_mhz, peak_src = measured_peaks()
+        perms_per_s = value                      # one Keccak-f[1600] per 64-byte SHA3-256 message
+        achieved = perms_per_s / world * INSTR_PER_PERMUTATION / 1e12   # per GPU
+        nominal_peak = 148 * 64 * sm_max_mhz * 1e6 / 1e12
+        probe = None
+        if not args.no_probe:
+            rate, hz = engine.probe_pipe(2)      # LOP3+SHF 2:1, the Keccak ALU mix
+            probe = {"instr_per_s": rate, "sm_hz": hz}
+        peak = probe["instr_per_s"] / 1e12 if probe else nominal_peak
+        per_launch = count
+        line = {
+            "metric": METRIC, "value": value, "unit": "hashes/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": seconds / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (reference generate_workload stream, seed 1, generated on device)",
+            "config": {"workload": f"SHA3-256 over 2^{args.log2_messages} x 64-byte messages sharded "
+                                   f"over {world} GPU(s) by contiguous ranges (BASELINE.json configs[4])",
+                       "messages_total": total, "messages_per_gpu": count, "message_bytes": MSG_LEN,
+                       "l2_policy": "inputs larger than L2 (%.1f GiB per GPU per step)" % (count * MSG_LEN / 2**30),
+                       "kernel": "hash_oneblock_kernel<17,8,8,UNROLL=24,ALU-only>"},
+            "gb_per_s_hashed": value * MSG_LEN / 1e9,
+            "gpu_launches": launches,
+            "digest_checksum": f"{checksum:016x}",
+            "clocks": clocks,
+            "roofline": {
+                "bound": "int_alu",
+                "achieved": achieved, "peak": peak, "unit": "Tinstr/s", "frac": achieved / peak,
+                "traffic": ncu_traffic_per_launch(per_launch),
+                "note": "per GPU; achieved = permutations/s x 4320 LOP3+SHF thread-instructions "
+                        "(SURVEY.md 8(d)); peak = LOP3+SHF issue rate measured in this run by "
+                        "b200sha3_probe_pipe" + ("" if probe else " [probe skipped: nominal]"),
+                "peak_nominal": nominal_peak,
+                "probe_sm_mhz": probe["sm_hz"] / 1e6 if probe else None,
+            },
+            "roofline_hbm": {
+                "bound": "hbm", "achieved": value / world * (MSG_LEN + DIGEST_BYTES) / 1e9,
+                "peak": hbm_peak, "unit": "GB/s",
+                "frac": value / world * (MSG_LEN + DIGEST_BYTES) / 1e9 / hbm_peak,
+                "peak_source": peak_src,
+                "note": "secondary: 96 algorithmic bytes per message; not the binding roofline",
+            },
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"], _ = cpu_baseline(args.cpu_log2_messages, 5, 1)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
