@@ -144,14 +144,9 @@ def cpu_baseline(log2_messages: int, steps: int, warmup: int):
     count = 1 << log2_messages
     total_bytes = (1 << 28) * MSG_LEN            # the stream of the full workload; we take its head
     oracle = Oracle()
-    # head of the full-size stream: same seed derivation as the GPU arm (seed ^ total*gamma,
-    # workload.cpp:34); word n of the stream is splitmix64 output number n
-    import numpy as np
-    data = np.zeros(count * MSG_LEN, dtype=np.uint8)
-    state_seed = (1 ^ (total_bytes * 0x9e3779b97f4a7c15)) & (2**64 - 1)
-    from paper_1902_05320_b200.engine import splitmix64_at
-    words = splitmix64_at(np.uint64(state_seed), np.arange(1, count * 8 + 1, dtype=np.uint64))
-    data[:] = words.view(np.uint8)
+    # head of the full-size stream (same seed derivation as the GPU arm: workload.cpp:34)
+    from paper_1902_05320_b200.sharding import workload_slice
+    data = workload_slice(total_bytes, MSG_LEN, 0, count, seed=1)
     cores = os.cpu_count() or 1
     if Reference.available():
         ref = Reference()
@@ -230,23 +225,20 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
+    from paper_1902_05320_b200.sharding import max_over_ranks as _max_over_ranks, shard_range
+
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return _max_over_ranks(x, device="cuda")
 
     total = 1 << args.log2_messages
     total_bytes = total * MSG_LEN
     # contiguous message range per rank (plan_partition analogue, batch.cpp:46-62)
-    first = total * rank // world
-    count = total * (rank + 1) // world - first
+    first, count = shard_range(total, rank, world)
 
     engine = Engine(device=local_rank)
     data = engine.generate_workload(total_bytes, MSG_LEN, seed=1, first_message=first, count=count)
@@ -270,14 +262,12 @@ def main():
     launches = engine.total_kernel_launches - launches_before
     value = total * args.steps / seconds
 
-    # checksum of this rank's digests: proves the timed kernels did the work (and lets a
-    # reader compare runs at different N: the XOR over ranks is N-independent)
-    fold = digests.view(torch.int64).view(-1)
-    checksum = int(torch.bitwise_xor(fold[0::2], fold[1::2]).sum().item()) & (2**64 - 1)
+    # checksum of the digests: sum of their 64-bit words mod 2^64 -- proves the timed
+    # kernels did the work, and is the same number for every N (sum over ranks)
+    t = digests.view(torch.int64).sum().reshape(1)
     if world > 1:
-        t = torch.tensor([checksum >> 1], dtype=torch.int64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        checksum = int(t.item())
+    checksum = int(t.item()) & (2**64 - 1)
 
     # ---- end to end through the host-buffer C entry (pinned host memory) -----------
     e2e = None

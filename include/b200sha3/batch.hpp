@@ -1,0 +1,103 @@
+// b200sha3/batch.hpp -- C++ adapter: the reference's batch interface over the
+// B200 engine.
+//
+// Mirrors proj/core/include/sha3/batch.hpp:13-65 of the reference: the same
+// HashBatch / BatchResult / EngineConfig shapes, the same contract for
+// hash_batch (order preserved, digests[i] belongs to messages[i], XOF without a
+// length throws std::invalid_argument before any work, empty batch -> empty
+// result, blocking and reentrant).  What differs is where the work happens:
+// messages are packed into one buffer, hashed by libb200sha3.so on the GPU
+// through the C ABI (include/b200sha3.h), and unpacked.
+//
+// Two ways to use it:
+//   * next to the reference's headers: define B200SHA3_USE_REFERENCE_TYPES
+//     before including this file; it then includes the reference's own
+//     "sha3/batch.hpp" and adds sha3::b200::hash_batch on those types;
+//   * instead of them: the types below are layout- and name-compatible
+//     declarations, and linking b200sha3_dropin.cpp (host/) provides
+//     sha3::hash_batch itself, replacing proj/core/src/batch.cpp at link time.
+#pragma once
+
+#include <chrono>
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <vector>
+
+#include "../b200sha3.h"
+
+#ifdef B200SHA3_USE_REFERENCE_TYPES
+#include "sha3/batch.hpp"
+#else
+namespace sha3 {
+
+// Enum order is the C ABI's algorithm id (proj/core/include/sha3/sha3.hpp:15-22).
+enum class Algorithm { sha3_224, sha3_256, sha3_384, sha3_512, shake128, shake256 };
+
+enum class Backend { sequential, parallel };
+
+// proj/core/include/sha3/batch.hpp:15-19.  On the GPU engine `workers` sizes the
+// host-side pack/unpack thread pool (0 = one per hardware thread); `backend`
+// and `chunk_size` have no device meaning and are accepted for compatibility.
+struct EngineConfig {
+  Backend backend = Backend::parallel;
+  unsigned workers = 0;
+  std::size_t chunk_size = 0;
+};
+
+// proj/core/include/sha3/batch.hpp:23-27
+struct HashBatch {
+  Algorithm algorithm = Algorithm::sha3_256;
+  std::vector<std::vector<std::uint8_t>> messages;
+  std::uint64_t xof_output_bits = 0;  // required for XOF variants
+};
+
+// proj/core/include/sha3/batch.hpp:29-34
+struct BatchResult {
+  std::vector<std::vector<std::uint8_t>> digests;  // digests[i] is the digest of messages[i]
+  std::chrono::duration<double> elapsed{0};        // hashing phase only
+};
+
+}  // namespace sha3
+#endif  // B200SHA3_USE_REFERENCE_TYPES
+
+namespace sha3::b200 {
+
+// Raised for CUDA failures and unsupported shapes (the C ABI's ERR_CUDA /
+// ERR_UNSUPPORTED).  Invalid arguments raise std::invalid_argument like the
+// reference (proj/core/src/batch.cpp:66-68).
+class DeviceError : public std::runtime_error {
+ public:
+  DeviceError(int status, const std::string& what) : std::runtime_error(what), status_(status) {}
+  int status() const { return status_; }
+
+ private:
+  int status_;
+};
+
+// Device-side knobs that EngineConfig has no field for.
+struct DeviceConfig {
+  int device = -1;           // CUDA ordinal, -1 = current
+  void* stream = nullptr;    // cudaStream_t
+  std::uint32_t flags = 0;   // B200SHA3_FLAG_*
+  int kernel = 0;            // B200SHA3_KERNEL_*
+};
+
+// Drop-in for sha3::hash_batch (proj/core/src/batch.cpp:64-135).
+// BatchResult::elapsed is the device time of the hashing kernels; packing,
+// copies and unpacking are outside it, as slot allocation and table warm-up
+// are outside the reference's timed region (batch.cpp:77-84, :133).
+BatchResult hash_batch(const HashBatch& batch, const EngineConfig& config = {},
+                       const DeviceConfig& device = {});
+
+// The same call on an already packed batch (what the adapter does internally):
+// message i is data[offsets[i], offsets[i] + lengths[i]).  Returns
+// count * digest_bytes bytes in message order.
+std::vector<std::uint8_t> hash_packed(Algorithm algorithm, const std::uint8_t* data,
+                                      const std::uint64_t* offsets,
+                                      const std::uint64_t* lengths, std::uint64_t count,
+                                      std::uint64_t xof_output_bits = 0,
+                                      const DeviceConfig& device = {},
+                                      double* elapsed_seconds = nullptr);
+
+}  // namespace sha3::b200

@@ -1,0 +1,136 @@
+// batch_adapter.cpp -- sha3::b200::hash_batch: pack -> C ABI -> unpack.
+//
+// Host-side mirror of the reference's hash_batch (proj/core/src/batch.cpp:64-135).
+// The only computation here is memcpy; every digest comes from libb200sha3.so.
+#include "b200sha3/batch.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <thread>
+
+namespace sha3::b200 {
+
+namespace {
+
+unsigned resolve_workers(const EngineConfig& config) {  // batch.cpp:38-44
+  if (config.workers > 0) return config.workers;
+  const unsigned hw = std::thread::hardware_concurrency();
+  return hw > 0 ? hw : 1;
+}
+
+// Runs fn(begin, end) over [0, n) split into contiguous ranges, one per worker
+// (the caller participates, like batch.cpp:126).
+template <class Fn>
+void parallel_ranges(std::size_t n, unsigned workers, std::uint64_t bytes, Fn fn) {
+  if (workers <= 1 || n < 2 || bytes < (8u << 20)) {
+    fn(std::size_t{0}, n);
+    return;
+  }
+  workers = static_cast<unsigned>(std::min<std::size_t>(workers, n));
+  std::vector<std::thread> pool;
+  pool.reserve(workers - 1);
+  for (unsigned w = 1; w < workers; ++w) {
+    pool.emplace_back(fn, n * w / workers, n * (w + 1) / workers);
+  }
+  fn(std::size_t{0}, n / workers);
+  for (auto& t : pool) t.join();
+}
+
+[[noreturn]] void raise(int status) {
+  if (status == B200SHA3_ERR_INVALID_ARGUMENT) {
+    // same message as the reference (batch.cpp:67)
+    throw std::invalid_argument("hash_batch: XOF variants need xof_output_bits");
+  }
+  throw DeviceError(status, std::string("b200sha3: ") + b200sha3_strerror(status) + ": " +
+                                b200sha3_last_cuda_error());
+}
+
+b200sha3_config make_config(const DeviceConfig& device, double* ms) {
+  b200sha3_config cfg{};
+  cfg.struct_size = sizeof cfg;
+  cfg.device = device.device;
+  cfg.stream = device.stream;
+  cfg.flags = device.flags;
+  cfg.kernel = device.kernel;
+  cfg.fma_preset = -1;
+  cfg.device_ms = ms;
+  return cfg;
+}
+
+}  // namespace
+
+std::vector<std::uint8_t> hash_packed(Algorithm algorithm, const std::uint8_t* data,
+                                      const std::uint64_t* offsets,
+                                      const std::uint64_t* lengths, std::uint64_t count,
+                                      std::uint64_t xof_output_bits, const DeviceConfig& device,
+                                      double* elapsed_seconds) {
+  const int alg = static_cast<int>(algorithm);
+  double ms = 0.0;
+  b200sha3_config cfg = make_config(device, &ms);
+  std::vector<std::uint8_t> out(count * b200sha3_digest_bytes(alg, xof_output_bits));
+  const int rc = b200sha3_hash_batch(alg, data, offsets, lengths, count, xof_output_bits,
+                                     out.data(), &cfg);
+  if (rc != B200SHA3_OK) raise(rc);
+  if (elapsed_seconds) *elapsed_seconds = ms * 1e-3;
+  return out;
+}
+
+BatchResult hash_batch(const HashBatch& batch, const EngineConfig& config,
+                       const DeviceConfig& device) {
+  const int alg = static_cast<int>(batch.algorithm);
+  // Validation first, before any allocation or copy (batch.cpp:66-68).
+  const bool is_xof = alg == B200SHA3_SHAKE128 || alg == B200SHA3_SHAKE256;
+  if (alg < 0 || alg > 5) throw std::invalid_argument("hash_batch: unknown algorithm");
+  if (is_xof && batch.xof_output_bits == 0) raise(B200SHA3_ERR_INVALID_ARGUMENT);
+
+  const std::size_t count = batch.messages.size();
+  const std::uint64_t digest_bytes = b200sha3_digest_bytes(alg, batch.xof_output_bits);
+  BatchResult result;
+  result.digests.resize(count);
+  if (count == 0) return result;  // test_batch.cpp:113-117
+  const unsigned workers = resolve_workers(config);
+
+  // Pack: offsets are an 8-byte aligned running sum so the device can use
+  // aligned 64-bit loads; equal lengths that are a multiple of 8 need no
+  // offset table at all (the fixed-length entry).
+  std::vector<std::uint64_t> offsets(count), lengths(count);
+  std::uint64_t total = 0;
+  bool fixed = true;
+  const std::uint64_t first_len = batch.messages[0].size();
+  for (std::size_t i = 0; i < count; ++i) {
+    const std::uint64_t len = batch.messages[i].size();
+    offsets[i] = total;
+    lengths[i] = len;
+    fixed = fixed && len == first_len;
+    total += (len + 7) & ~std::uint64_t{7};
+  }
+  fixed = fixed && (first_len % 8 == 0 || count == 1);
+  std::vector<std::uint8_t> data(std::max<std::uint64_t>(total, 16));
+  parallel_ranges(count, workers, total, [&](std::size_t begin, std::size_t end) {
+    for (std::size_t i = begin; i < end; ++i) {
+      if (lengths[i]) std::memcpy(data.data() + offsets[i], batch.messages[i].data(), lengths[i]);
+    }
+  });
+
+  std::vector<std::uint8_t> packed(count * digest_bytes);
+  double ms = 0.0;
+  b200sha3_config cfg = make_config(device, &ms);
+  const int rc =
+      fixed ? b200sha3_hash_fixed(alg, data.data(), first_len, count, batch.xof_output_bits,
+                                  packed.data(), &cfg)
+            : b200sha3_hash_batch(alg, data.data(), offsets.data(), lengths.data(), count,
+                                  batch.xof_output_bits, packed.data(), &cfg);
+  if (rc != B200SHA3_OK) raise(rc);
+
+  parallel_ranges(count, workers, count * digest_bytes, [&](std::size_t begin, std::size_t end) {
+    for (std::size_t i = begin; i < end; ++i) {
+      const std::uint8_t* d = packed.data() + i * digest_bytes;
+      result.digests[i].assign(d, d + digest_bytes);
+    }
+  });
+  result.elapsed = std::chrono::duration<double>(ms * 1e-3);
+  return result;
+}
+
+}  // namespace sha3::b200

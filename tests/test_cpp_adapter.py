@@ -1,0 +1,34 @@
+"""Builds and runs tests/cpp/test_batch_adapter (the reference's test_batch.cpp
+hash_batch cases restated against the C++ adapter / sha3::hash_batch drop-in)."""
+import pathlib
+import subprocess
+
+import pytest
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+EXE = ROOT / "tests" / "cpp" / "test_batch_adapter"
+
+
+def build():
+    subprocess.run(["make", "-C", str(ROOT / "paper_1902_05320_b200" / "host")], check=True,
+                   stdout=subprocess.DEVNULL)
+    subprocess.run(["make", "-C", str(ROOT / "oracle"), "liboracle.so"], check=True,
+                   stdout=subprocess.DEVNULL)
+    subprocess.run(["make", "-C", str(ROOT / "tests" / "cpp")], check=True, stdout=subprocess.DEVNULL)
+
+
+def test_adapter_cpu_only_cases():
+    """XOF-without-length throws std::invalid_argument with the reference's message before
+    any work; an empty batch gives an empty result -- no device needed."""
+    build()
+    out = subprocess.run([str(EXE), "--cpu-only"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "0 failures" in out.stdout
+
+
+@pytest.mark.gpu
+def test_adapter_all_cases():
+    build()
+    out = subprocess.run([str(EXE)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "0 failures" in out.stdout
