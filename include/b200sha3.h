@@ -206,7 +206,10 @@ B200SHA3_API int b200sha3_bucket_order_device(int algorithm, const uint64_t* d_l
  * clock seen (cycles of clock64 per second of globaltimer) through *sm_hz.
  * mix: 0 LOP3, 1 SHF, 2 LOP3+SHF 2:1 (the Keccak ALU mix), 3 IMAD, 4 IMAD.WIDE,
  *      5 IMAD.HI, 6 LOP3+IMAD 1:1, 7 LOP3+IMAD.WIDE 1:1, 8 LOP3+IMAD.HI 1:1,
- *      9 (LOP3+SHF 2:1) + the 3-op FMA rotate group. */
+ *      9 the flavour-2 Keccak mix (5 LOP3 : 2 IMAD : 2 IMAD.HI);
+ *      10..15 the same with realistic operand traffic (three distinct registers per
+ *      LOP3): 10 LOP3, 11 LOP3+IMAD 1:1, 12 LOP3+IMAD 3:1, 13 LOP3+IMAD(1 reg) 3:1,
+ *      14 LOP3+IMAD.HI 3:1, 15 LOP3+SHF 2:1. */
 B200SHA3_API int b200sha3_probe_pipe(int mix, double* instr_per_s, double* sm_hz,
                                      const b200sha3_config* cfg);
 

@@ -623,7 +623,7 @@ int b200sha3_bucket_order_device(int algorithm, const uint64_t* d_lengths, uint6
 
 int b200sha3_probe_pipe(int mix, double* instr_per_s, double* sm_hz,
                         const b200sha3_config* cfg) {
-  if (mix < 0 || mix > 9) return B200SHA3_ERR_INVALID_ARGUMENT;
+  if (mix < 0 || mix > 15) return B200SHA3_ERR_INVALID_ARGUMENT;
   const Config c = resolve(cfg);
   DeviceGuard guard;
   CU(guard.enter(c.device));

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(256) probe_kernel(uint32_t seed, uint32_t mult
   uint32_t b0 = a0 ^ 0x1234u, b1 = a1 ^ 0x77u, b2 = a2 ^ 0x99u, b3 = a3 ^ 0x4321u;
   uint32_t c0 = a0 + 11u, c1 = a1 + 13u, c2 = a2 + 17u, c3 = a3 + 19u;
   uint64_t w0 = a0, w1 = a1, w2 = a2, w3 = a3;
+  uint32_t pool[12] = {a0, a1, a2, a3, b0, b1, b2, b3, c0, c1, c2, c3};
   const uint32_t y = seed * 0x9e3779b9u + 1u, z = ~seed;
   const uint32_t m = mult;  // runtime value (a power of two), opaque to ptxas
   const long long t0 = clock64();
@@ -82,6 +83,34 @@ __global__ void __launch_bounds__(256) probe_kernel(uint32_t seed, uint32_t mult
       } else if constexpr (MIX == 8) {  // 4 LOP3 + 4 IMAD.HI
         LOP(a0, y, z); MULHI(b0, m); LOP(a1, y, z); MULHI(b1, m);
         LOP(a2, y, z); MULHI(b2, m); LOP(a3, y, z); MULHI(b3, m);
+      } else if constexpr (MIX >= 10) {
+        // Realistic operand traffic: a pool of 12 registers, every one rewritten every 12
+        // steps; each LOP3 reads three distinct pool registers (like theta / chi do), and
+        // the interleaved second instruction reads pool registers too.
+        //   10: LOP3 only              11: LOP3 + IMAD(r,c,r) 1:1     12: LOP3 + IMAD(r,c,r) 3:1
+        //   13: LOP3 + IMAD(r,c,RZ) 3:1   14: LOP3 + IMAD.HI(r,c,RZ) 3:1   15: LOP3 + SHF 2:1
+#pragma unroll
+        for (int k = 0; k < 12; ++k) {
+          asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;"
+                       : "=r"(pool[k])
+                       : "r"(pool[(k + 1) % 12]), "r"(pool[(k + 5) % 12]), "r"(pool[(k + 8) % 12]));
+          const bool second = (MIX == 11) || (MIX >= 12 && MIX <= 14 && k % 3 == 2) ||
+                              (MIX == 15 && k % 2 == 1);
+          if (second) {
+            const int j = (k + 6) % 12;
+            if constexpr (MIX == 11 || MIX == 12) {
+              asm volatile("mad.lo.u32 %0, %1, %2, %3;"
+                           : "=r"(pool[j]) : "r"(pool[(j + 2) % 12]), "r"(m), "r"(pool[(j + 7) % 12]));
+            } else if constexpr (MIX == 13) {
+              asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(pool[j]) : "r"(pool[(j + 2) % 12]), "r"(m));
+            } else if constexpr (MIX == 14) {
+              asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(pool[j]) : "r"(pool[(j + 2) % 12]), "r"(m));
+            } else {
+              asm volatile("shf.l.wrap.b32 %0, %1, %2, 7;"
+                           : "=r"(pool[j]) : "r"(pool[(j + 2) % 12]), "r"(pool[(j + 7) % 12]));
+            }
+          }
+        }
       } else {  // 9: the flavour-2 Keccak mix, 5 LOP3 : 2 IMAD : 2 IMAD.HI (+ 1 SHF per 2)
         LOP(a0, y, z); LOP(a1, y, z); MAD(b0, m, y); MULHI(c0, m); LOP(a2, y, z);
         LOP(a3, y, z); MAD(b1, m, y); MULHI(c1, m); LOP(b2, y, z);
@@ -90,7 +119,10 @@ __global__ void __launch_bounds__(256) probe_kernel(uint32_t seed, uint32_t mult
   }
   const uint64_t g1 = global_timer_ns();
   const long long t1 = clock64();
-  const uint32_t r = a0 ^ a1 ^ a2 ^ a3 ^ b0 ^ b1 ^ b2 ^ b3 ^ c0 ^ c1 ^ c2 ^ c3 ^
+  uint32_t pr = 0;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) pr ^= pool[k];
+  const uint32_t r = pr ^ a0 ^ a1 ^ a2 ^ a3 ^ b0 ^ b1 ^ b2 ^ b3 ^ c0 ^ c1 ^ c2 ^ c3 ^
                      static_cast<uint32_t>(w0 ^ w1 ^ w2 ^ w3) ^
                      static_cast<uint32_t>((w0 ^ w1 ^ w2 ^ w3) >> 32);
   if (r == 0x5a5a5a5au) sink[0] = r;  // keeps the chains alive
@@ -101,7 +133,8 @@ __global__ void __launch_bounds__(256) probe_kernel(uint32_t seed, uint32_t mult
 }
 
 // MADWIDE counts as two instructions (IMAD.WIDE + IMAD).
-constexpr int kInstrPerUnroll[10] = {8, 8, 12, 8, 16, 8, 8, 12, 8, 9};
+constexpr int kProbeMixes = 16;
+constexpr int kInstrPerUnroll[kProbeMixes] = {8, 8, 12, 8, 16, 8, 8, 12, 8, 9, 12, 24, 16, 16, 16, 18};
 
 template <int MIX>
 cudaError_t launch_probe(unsigned blocks, uint32_t* sink, uint64_t* timing, cudaStream_t s) {
@@ -122,6 +155,12 @@ cudaError_t launch_mix(int mix, unsigned blocks, uint32_t* sink, uint64_t* timin
     case 7: return launch_probe<7>(blocks, sink, timing, s);
     case 8: return launch_probe<8>(blocks, sink, timing, s);
     case 9: return launch_probe<9>(blocks, sink, timing, s);
+    case 10: return launch_probe<10>(blocks, sink, timing, s);
+    case 11: return launch_probe<11>(blocks, sink, timing, s);
+    case 12: return launch_probe<12>(blocks, sink, timing, s);
+    case 13: return launch_probe<13>(blocks, sink, timing, s);
+    case 14: return launch_probe<14>(blocks, sink, timing, s);
+    case 15: return launch_probe<15>(blocks, sink, timing, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -129,7 +168,7 @@ cudaError_t launch_mix(int mix, unsigned blocks, uint32_t* sink, uint64_t* timin
 }  // namespace
 
 cudaError_t run_pipe_probe(int mix, double* instr_per_s, double* sm_hz, cudaStream_t stream) {
-  if (mix < 0 || mix > 9) return cudaErrorInvalidValue;
+  if (mix < 0 || mix >= kProbeMixes) return cudaErrorInvalidValue;
   int dev = 0, sms = 0;
   cudaError_t err = cudaGetDevice(&dev);
   if (err != cudaSuccess) return err;

@@ -201,6 +201,42 @@ def test_every_kernel_variant_agrees(engine, oracle):
     assert (got.cpu().numpy() == expect_xof).all()
 
 
+@pytest.mark.parametrize("algorithm,msg_len,bits", [
+    (0, 32, 0), (0, 64, 0), (0, 128, 0), (1, 32, 0), (1, 64, 0), (1, 128, 0), (2, 32, 0), (2, 64, 0),
+    (3, 32, 0), (3, 64, 0), (4, 32, 256), (4, 64, 256), (4, 128, 256), (4, 64, 512), (5, 64, 256),
+    (5, 64, 512), (5, 32, 256), (5, 128, 256)])
+def test_oneblock_shapes(oracle, algorithm, msg_len, bits):
+    """Every instantiated shape of the single-block kernel, forced, vs the oracle; shapes
+    without an instantiation must be refused (no silent substitution)."""
+    import torch
+    from paper_1902_05320_b200 import Engine, EngineError
+    from paper_1902_05320_b200.engine import KERNEL_ONEBLOCK
+    count = 4097
+    host = oracle.generate_workload(count * msg_len, msg_len, seed=21)
+    dev = torch.from_numpy(host).cuda()
+    expect = oracle.hash_batch(algorithm, host, fixed_len=msg_len, count=count, xof_bits=bits, workers=4)
+    got = Engine(kernel=KERNEL_ONEBLOCK).hash_fixed(algorithm, dev, msg_len, count, bits)
+    assert (got.cpu().numpy() == expect).all()
+    with pytest.raises(EngineError):
+        Engine(kernel=KERNEL_ONEBLOCK).hash_fixed(algorithm, dev[:count * 24].contiguous(), 24, count, bits)
+
+
+@pytest.mark.parametrize("algorithm,msg_len,bits", [(1, 64, 0), (1, 8, 0), (1, 128, 0), (3, 64, 0),
+                                                    (2, 96, 0), (5, 64, 512), (4, 160, 1344)])
+def test_lanesplit_kernel(oracle, algorithm, msg_len, bits):
+    """The lane-split comparison kernel (5 threads per state, shuffles + shared tile) gives
+    the same digests; counts that do not fill the last warp / block included."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import KERNEL_LANESPLIT
+    for count in (1, 5, 6, 7, 24, 25, 10_007):
+        host = oracle.generate_workload(count * msg_len, msg_len, seed=31)
+        dev = torch.from_numpy(np.concatenate([host, np.zeros(16, np.uint8)])).cuda()
+        expect = oracle.hash_batch(algorithm, host, fixed_len=msg_len, count=count, xof_bits=bits)
+        got = Engine(kernel=KERNEL_LANESPLIT).hash_fixed(algorithm, dev, msg_len, count, bits)
+        assert (got.cpu().numpy() == expect).all(), count
+
+
 def test_bucket_order_is_a_sorted_permutation(engine):
     """Device bucketing: every index exactly once, block counts non-increasing
     up to the bin width."""

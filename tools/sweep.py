@@ -15,7 +15,9 @@ from paper_1902_05320_b200 import Engine  # noqa: E402
 from paper_1902_05320_b200.engine import KERNEL_GENERIC, KERNEL_ONEBLOCK  # noqa: E402
 
 MIXES = ["LOP3", "SHF", "LOP3+SHF 2:1", "IMAD", "IMAD.WIDE+IMAD", "IMAD.HI", "LOP3+IMAD 1:1",
-         "LOP3+(IMAD.WIDE+IMAD)", "LOP3+IMAD.HI 1:1", "keccak flavour-2 mix"]
+         "LOP3+(IMAD.WIDE+IMAD)", "LOP3+IMAD.HI 1:1", "keccak flavour-2 mix",
+         "pool LOP3", "pool LOP3+IMAD 1:1", "pool LOP3+IMAD 3:1", "pool LOP3+IMAD(1reg) 3:1",
+         "pool LOP3+IMAD.HI 3:1", "pool LOP3+SHF 2:1"]
 
 
 def time_hash(engine, dev, count, reps=5, msg_len=64, alg="sha3_256", bits=0):
@@ -54,6 +56,14 @@ def main():
                            "ms": ms, "ghash_per_s": count / ms / 1e6, "ok": ok}
                     res["variants"].append(rec)
                     print(rec, flush=True)
+    from paper_1902_05320_b200.engine import KERNEL_LANESPLIT
+    eng = Engine(kernel=KERNEL_LANESPLIT)
+    ms = time_hash(eng, dev, count, reps=3)
+    ok = bool(torch.equal(eng.hash_fixed("sha3_256", dev, 64, count), ref))
+    rec = {"kernel": "lanesplit", "unroll": 1, "fma_preset": 0, "threads": 128, "ms": ms,
+           "ghash_per_s": count / ms / 1e6, "ok": ok}
+    res["variants"].append(rec)
+    print(rec, flush=True)
     (out_dir / "sweep.json").write_text(json.dumps(res, indent=1))
 
 
