@@ -209,19 +209,33 @@ __device__ __forceinline__ void keccak_round(State& a, uint32_t rc_lo, uint32_t 
 
 #undef B200SHA3_RHOPI
 
-// 24 rounds.  UNROLL = 24 uses immediates (and lets ptxas drop work on lanes
-// that are known zero on entry or dead on exit); smaller values keep the body
-// I-cache resident and read the constants from the constant bank.
+// 24 rounds.
+//   UNROLL = 24  straight-line code with immediates; ptxas also drops the work on lanes
+//                that are known zero on entry and on lanes nobody reads on exit.
+//   UNROLL = 22  "peeled": rounds 0 and 23 straight-line (so the same dead-work removal
+//                applies to them), rounds 1..22 in a loop of two rounds per body that
+//                stays I-cache resident (the 67 KB fully unrolled body does not).
+//   UNROLL = 1, 2, 4  plain loop, constants from the constant bank.
 template <int UNROLL, uint32_t FMA_MASK>
 __device__ __forceinline__ void keccak_f1600(State& a) {
-  static_assert(24 % UNROLL == 0, "UNROLL must divide 24");
   if constexpr (UNROLL == 24) {
 #pragma unroll
     for (int r = 0; r < 24; ++r) {
       keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(r)),
                              static_cast<uint32_t>(round_constant(r) >> 32));
     }
+  } else if constexpr (UNROLL == 22) {
+    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(0)),
+                           static_cast<uint32_t>(round_constant(0) >> 32));
+#pragma unroll 1
+    for (int r = 1; r < 23; r += 2) {
+      keccak_round<FMA_MASK>(a, kRoundConst32[2 * r], kRoundConst32[2 * r + 1]);
+      keccak_round<FMA_MASK>(a, kRoundConst32[2 * r + 2], kRoundConst32[2 * r + 3]);
+    }
+    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(23)),
+                           static_cast<uint32_t>(round_constant(23) >> 32));
   } else {
+    static_assert(24 % UNROLL == 0, "UNROLL must divide 24");
 #pragma unroll 1
     for (int r = 0; r < 24; r += UNROLL) {
 #pragma unroll
