@@ -48,6 +48,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    # validation only (one-GPU box): run N ranks on the SAME device with a gloo process group
+    # to exercise the multi-rank code path; numbers from such a run are not benchmark values
+    ap.add_argument("--share-gpu", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -221,9 +224,15 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch with torch.distributed.run")
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    if args.share_gpu:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
+    reduce_device = "cpu" if args.share_gpu else "cuda"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     from paper_1902_05320_b200.sharding import max_over_ranks as _max_over_ranks, shard_range
 
@@ -233,7 +242,7 @@ def main():
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        return _max_over_ranks(x, device="cuda")
+        return _max_over_ranks(x, device=reduce_device)
 
     total = 1 << args.log2_messages
     total_bytes = total * MSG_LEN
@@ -264,7 +273,7 @@ def main():
 
     # checksum of the digests: sum of their 64-bit words mod 2^64 -- proves the timed
     # kernels did the work, and is the same number for every N (sum over ranks)
-    t = digests.view(torch.int64).sum().reshape(1)
+    t = digests.view(torch.int64).sum().reshape(1).to(reduce_device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
     checksum = int(t.item()) & (2**64 - 1)
@@ -309,6 +318,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": seconds / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (reference generate_workload stream, seed 1, generated on device)",
+            **({"validation_only": "ranks share one GPU (gloo); not a benchmark value"} if args.share_gpu else {}),
             "config": {"workload": f"SHA3-256 over 2^{args.log2_messages} x 64-byte messages sharded "
                                    f"over {world} GPU(s) by contiguous ranges (BASELINE.json configs[4])",
                        "messages_total": total, "messages_per_gpu": count, "message_bytes": MSG_LEN,

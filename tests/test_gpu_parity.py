@@ -360,3 +360,96 @@ def test_reentrant_from_multiple_callers(engine, oracle):
 def test_xof_without_length_rejected_on_gpu_box_too(engine):
     with pytest.raises(ValueError):
         engine.hash_messages("shake256", [b"\x01"], 0)
+
+
+# ---- BASELINE.json configs at FULL size, through size-independent properties ----------
+
+def _sample_check(oracle, algorithm, dev, msg_len, count, digests, bits=0, n=2048, seed=9):
+    import torch
+    idx = torch.randint(0, count, (n,), generator=torch.Generator().manual_seed(seed)).cuda()
+    msgs = dev.view(count, msg_len)[idx].cpu().numpy()
+    expect = oracle.hash_batch(algorithm, msgs, fixed_len=msg_len, count=n, xof_bits=bits, workers=8)
+    assert (digests[idx].cpu().numpy() == expect).all()
+
+
+def test_cfg5_full_size_2pow28(engine, oracle):
+    """configs[4]: SHA3-256 over 2^28 x 64 B (16 GiB in, 8 GiB out).  Two independent kernels
+    (single-block, fully unrolled vs generic, rolled) agree on every digest; 2048 sampled
+    messages match the oracle; eight independently generated shards reproduce the digests
+    (the N-GPU invariance); the first message is the cfg1/cfg5 stream KAT."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import KERNEL_GENERIC
+    count = 1 << 28
+    dev = engine.generate_workload(count * 64, 64, seed=1)
+    fast = engine.hash_fixed("sha3_256", dev, 64, count)
+    slow = Engine(kernel=KERNEL_GENERIC).hash_fixed("sha3_256", dev, 64, count)
+    assert torch.equal(fast, slow)
+    del slow
+    _sample_check(oracle, 1, dev, 64, count, fast)
+    whole = int(fast.view(torch.int64).sum().item())
+    parts = 0
+    for rank in range(8):
+        first, n = rank * (count // 8), count // 8
+        shard = engine.generate_workload(count * 64, 64, seed=1, first_message=first, count=n)
+        part = engine.hash_fixed("sha3_256", shard, 64, n)
+        if rank in (0, 5):
+            assert torch.equal(part, fast[first:first + n])
+        parts = (parts + int(part.view(torch.int64).sum().item())) & (2**64 - 1)
+        del shard, part
+    assert parts == whole & (2**64 - 1)
+
+
+@pytest.mark.parametrize("algorithm,msg_len,bits", [(0, 32, 0), (0, 1024, 0), (2, 256, 0), (3, 1024, 0),
+                                                    (4, 64, 4096), (5, 64, 256), (5, 64, 2048)])
+def test_cfg2_cfg3_full_size_2pow24(engine, oracle, algorithm, msg_len, bits):
+    """configs[1] / configs[2] at 2^24 messages: auto-selected kernel == generic kernel on all
+    digests, sampled oracle check, XOF prefix property (shorter output is a prefix)."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import KERNEL_GENERIC
+    count = 1 << 24
+    dev = engine.generate_workload(count * msg_len, msg_len, seed=1)
+    got = engine.hash_fixed(algorithm, dev, msg_len, count, bits)
+    _sample_check(oracle, algorithm, dev, msg_len, count, got, bits, n=512)
+    if msg_len <= 128:
+        other = Engine(kernel=KERNEL_GENERIC).hash_fixed(algorithm, dev, msg_len, count, bits)
+        assert torch.equal(got, other)
+    if algorithm >= 4 and bits > 256:
+        short = engine.hash_fixed(algorithm, dev, msg_len, count, 256)
+        assert torch.equal(short, got[:, :32])          # test_sha3.cpp:150-158 at scale
+
+
+def test_cfg4_full_size_2pow22(engine, oracle):
+    """configs[3]: 2^22 messages, lengths 1..16 KiB (~34 GB): bucketed and unbucketed runs
+    agree on every digest; 256 sampled messages match the oracle; digest slots follow input
+    order although processing order is by block count."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_BUCKETING
+    count = 1 << 22
+    lengths = engine.generate_lengths(count, 1, 16384, seed_len=2)
+    padded = (lengths + 7) // 8 * 8
+    offsets = torch.cumsum(padded, 0) - padded
+    data = torch.empty(int(padded.sum().item()) + 16, dtype=torch.uint8, device="cuda")
+    engine.fill_messages(data, offsets, lengths, seed=1)
+    a = engine.hash_batch("sha3_256", data, offsets, lengths)
+    b = Engine(flags=FLAG_NO_BUCKETING).hash_batch("sha3_256", data, offsets, lengths)
+    assert torch.equal(a, b)
+    idx = torch.randint(0, count, (256,), generator=torch.Generator().manual_seed(3))
+    for i in idx.tolist():
+        off, n = int(offsets[i].item()), int(lengths[i].item())
+        assert a[i].cpu().numpy().tobytes() == oracle.hash_one(1, data[off:off + n].cpu().numpy().tobytes())
+
+
+def test_one_huge_message_among_small_ones(engine):
+    """Maximum-size edge: a 64 MiB message (493k blocks: the clamped top bucket) next to tiny
+    ones, against hashlib (OpenSSL) -- the oracle's C loop would do too, hashlib is quicker."""
+    import hashlib
+    rng = np.random.default_rng(5)
+    big = rng.integers(0, 256, 64 * 1024 * 1024 + 5, dtype=np.uint8).tobytes()
+    msgs = [b"", big, b"abc", big[:136 * 300], bytes(200)]
+    for alg, name in ((1, "sha3_256"), (3, "sha3_512")):
+        assert engine.hash_messages(alg, msgs) == [hashlib.new(name, m).digest() for m in msgs]
+    got = engine.hash_messages("shake128", msgs[1:3], 1344 * 2 + 8)
+    assert got == [hashlib.shake_128(m).digest(337) for m in msgs[1:3]]

@@ -48,7 +48,7 @@ def main():
     for kernel, kname, unrolls in ((KERNEL_ONEBLOCK, "oneblock", (2, 22, 24)), (KERNEL_GENERIC, "generic", (2,))):
         for unroll in unrolls:
             for preset in ((0, 8) if kernel == KERNEL_ONEBLOCK else (0,)):
-                for threads in ((64, 128, 256, 512) if preset == 0 else (128,)):
+                for threads in ((64, 128, 256) if preset == 0 else (128,)):
                     eng = Engine(kernel=kernel, unroll=unroll, fma_preset=preset, block_threads=threads)
                     ms = time_hash(eng, dev, count)
                     ok = bool(torch.equal(eng.hash_fixed("sha3_256", dev, 64, count), ref))
