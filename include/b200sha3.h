@@ -145,6 +145,12 @@ B200SHA3_API int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_
                                      uint64_t count, uint64_t xof_output_bits,
                                      uint8_t* digests, const b200sha3_config* cfg);
 
+/* Page-locked (pinned, portable) host memory: buffers obtained here let the host entries
+ * above overlap their copies with compute at full PCIe speed; pageable memory works too,
+ * more slowly.  The C++ adapter packs into such buffers. */
+B200SHA3_API int b200sha3_pinned_alloc(uint64_t bytes, void** out);
+B200SHA3_API int b200sha3_pinned_free(void* ptr);
+
 /* ---- device-buffer entries ----------------------------------------------
  * All pointers are DEVICE pointers on cfg->device.  Work is enqueued on
  * cfg->stream and the call returns without waiting (unless cfg->device_ms is

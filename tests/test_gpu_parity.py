@@ -453,3 +453,45 @@ def test_one_huge_message_among_small_ones(engine):
         assert engine.hash_messages(alg, msgs) == [hashlib.new(name, m).digest() for m in msgs]
     got = engine.hash_messages("shake128", msgs[1:3], 1344 * 2 + 8)
     assert got == [hashlib.shake_128(m).digest(337) for m in msgs[1:3]]
+
+
+def test_variable_length_host_entry_pipelined(engine, oracle):
+    """Host entry, packed ragged batch of ~200 MB: chunked 3-slot pipeline == single shot ==
+    oracle (sampled); a batch whose offsets are NOT in order falls back to the single-shot
+    path and is still right; permuting the messages permutes the digests."""
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_PIPELINE
+    rng = np.random.default_rng(12)
+    count = 50_000
+    lengths = rng.integers(0, 8192, count).astype(np.uint64)
+    padded = (lengths + np.uint64(7)) // np.uint64(8) * np.uint64(8)
+    offsets = (np.cumsum(padded) - padded).astype(np.uint64)
+    data = rng.integers(0, 256, int(padded.sum()) + 16, dtype=np.uint8)
+    piped = engine.hash_batch("sha3_384", data, offsets, lengths)
+    single = Engine(flags=FLAG_NO_PIPELINE).hash_batch("sha3_384", data, offsets, lengths)
+    assert (piped == single).all()
+    sample = rng.choice(count, 300, replace=False)
+    for i in sample:
+        m = data[int(offsets[i]):int(offsets[i] + lengths[i])].tobytes()
+        assert piped[i].tobytes() == oracle.hash_one(2, m)
+    perm = rng.permutation(count)
+    shuffled = engine.hash_batch("sha3_384", data, offsets[perm], lengths[perm])   # offsets out of order
+    assert (shuffled == piped[perm]).all()
+
+
+def test_pinned_alloc_api(engine):
+    import ctypes as C
+    lib = engine.lib
+    lib.b200sha3_pinned_alloc.argtypes = [C.c_uint64, C.POINTER(C.c_void_p)]
+    lib.b200sha3_pinned_free.argtypes = [C.c_void_p]
+    p = C.c_void_p()
+    assert lib.b200sha3_pinned_alloc(1 << 20, C.byref(p)) == 0 and p.value
+    buf = (C.c_uint8 * 64).from_address(p.value)
+    for i in range(64):
+        buf[i] = i
+    out = np.zeros(32, dtype=np.uint8)
+    engine.hash_fixed_ptr("sha3_256", p.value, 64, 1, out.ctypes.data)
+    import hashlib
+    assert out.tobytes() == hashlib.sha3_256(bytes(range(64))).digest()
+    assert lib.b200sha3_pinned_free(p) == 0
+    assert lib.b200sha3_pinned_alloc(0, C.byref(p)) == 0 and not p.value
