@@ -58,7 +58,11 @@ enum {
   /* Any CUDA runtime failure (no device, out of memory, launch failure). */
   B200SHA3_ERR_CUDA = 2,
   /* Batch shape the engine cannot take (e.g. a single digest > 4 GiB). */
-  B200SHA3_ERR_UNSUPPORTED = 3
+  B200SHA3_ERR_UNSUPPORTED = 3,
+  /* Incremental API used out of order: update after finish, finish twice, squeeze before
+   * finish or on a fixed-output variant.  Maps to std::logic_error
+   * (proj/core/src/sponge.cpp:82-84, :114-116, :132-134; proj/core/src/sha3.cpp:103-126). */
+  B200SHA3_ERR_STATE = 4
 };
 
 /* Algorithm ids, reference enum order (sha3.hpp:15-22). */
@@ -98,8 +102,8 @@ typedef struct b200sha3_config {
   void* stream;            /* cudaStream_t to enqueue on; NULL = the default stream */
   uint32_t flags;          /* B200SHA3_FLAG_*                                        */
   int32_t kernel;          /* B200SHA3_KERNEL_*                                      */
-  int32_t unroll;          /* rounds per loop body: 0 = default, else 1,2,4 or 24    */
-  int32_t fma_preset;      /* -1 = default; 0..7 = FMA-pipe rotation offload preset  */
+  int32_t unroll;          /* one-block kernel: 0 = default, else 2, 4, 22 (peeled), 24 */
+  int32_t fma_preset;      /* -1 = default; 0..8 = FMA-pipe rotation offload preset  */
   int32_t block_threads;   /* 0 = default                                            */
   /* If non-NULL receives the device time of the hashing phase in milliseconds
    * (CUDA events around the kernels; copies excluded) -- what the adapter
@@ -205,6 +209,41 @@ B200SHA3_API int b200sha3_permute_device(uint64_t* d_states, uint64_t count,
 B200SHA3_API int b200sha3_bucket_order_device(int algorithm, const uint64_t* d_lengths,
                                               uint64_t count, uint32_t* d_order,
                                               const b200sha3_config* cfg);
+
+/* ---- batched incremental hashing (device) --------------------------------
+ * `count` independent sponge states resident in HBM, fed chunk by chunk: the batch
+ * analogue of sha3::Hasher (proj/core/include/sha3/sha3.hpp:66-86) over SpongeHasher
+ * (proj/core/include/sha3/sponge.hpp:38-64).  For inputs that do not fit one buffer or
+ * arrive in pieces.  Feeding a message in any chunking gives the one-shot digest
+ * (proj/tests/test_sponge.cpp:114-132); squeezing an XOF in pieces gives the one-shot
+ * output (proj/tests/test_sponge.cpp:134-150).  All pointers are device pointers; calls
+ * are asynchronous on cfg->stream.  A handle is single-owner (not for concurrent calls),
+ * like the reference's Hasher. */
+typedef struct b200sha3_states b200sha3_states;
+
+B200SHA3_API int b200sha3_states_create(int algorithm, uint64_t count,
+                                        const b200sha3_config* cfg, b200sha3_states** out);
+B200SHA3_API int b200sha3_states_destroy(b200sha3_states* states);
+/* Hasher::reset (sha3.cpp:128-130). */
+B200SHA3_API int b200sha3_states_reset(b200sha3_states* states, const b200sha3_config* cfg);
+/* Hasher::update: chunk i = d_data[d_offsets[i], +d_lengths[i]) goes to stream i
+ * (lengths may be 0). */
+B200SHA3_API int b200sha3_states_update_device(b200sha3_states* states, const uint8_t* d_data,
+                                               const uint64_t* d_offsets,
+                                               const uint64_t* d_lengths,
+                                               const b200sha3_config* cfg);
+/* Same with equal-length chunks back to back. */
+B200SHA3_API int b200sha3_states_update_fixed_device(b200sha3_states* states,
+                                                     const uint8_t* d_data, uint64_t chunk_len,
+                                                     const b200sha3_config* cfg);
+/* Hasher::digest (hash variants: d_digests required) / Hasher::finish + first read (XOF:
+ * xof_output_bits may be 0 to only close the input; otherwise ceil(bits/8) bytes per stream
+ * are written, last byte masked like batch.cpp:22-24). */
+B200SHA3_API int b200sha3_states_finish_device(b200sha3_states* states, uint64_t xof_output_bits,
+                                               uint8_t* d_digests, const b200sha3_config* cfg);
+/* Hasher::read: the next out_bytes bytes of every XOF stream, packed count x out_bytes. */
+B200SHA3_API int b200sha3_states_squeeze_device(b200sha3_states* states, uint64_t out_bytes,
+                                                uint8_t* d_out, const b200sha3_config* cfg);
 
 /* ---- pipe microbenchmark ---------------------------------------------------
  * Measures the issue rate of one instruction mix on the current device:

@@ -9,5 +9,5 @@ memory, streams and ``torch.distributed`` and nothing else.
 There is no CPU fallback: importing ``engine`` without the built library, or
 calling it without a CUDA device, raises.
 """
-from .engine import (ALGORITHMS, Engine, EngineError, algorithm_id, digest_bytes,  # noqa: F401
-                     library_path, permutations, rate_bytes)
+from .engine import (ALGORITHMS, BatchHasher, Engine, EngineError, EngineStateError,  # noqa: F401
+                     algorithm_id, digest_bytes, library_path, permutations, rate_bytes)

@@ -94,6 +94,17 @@ cudaError_t launch_fill_messages(uint64_t seed, uint64_t first_message, uint64_t
                                  const uint64_t* offsets, const uint64_t* lengths,
                                  uint8_t* data, cudaStream_t stream);
 
+// Batched incremental hashing (kernel_stream.cu): `lanes` is 25 * count uint2 (structure
+// of arrays), `pos` is count words.
+cudaError_t launch_states_update(int rate_lanes, void* lanes, uint32_t* pos, uint64_t count,
+                                 const uint8_t* data, const uint64_t* offsets,
+                                 const uint64_t* lengths, uint64_t fixed_len, cudaStream_t stream);
+cudaError_t launch_states_finish(int rate_lanes, void* lanes, uint32_t* pos, uint64_t count,
+                                 uint32_t head, uint8_t* out, uint64_t out_len, uint32_t last_mask,
+                                 cudaStream_t stream);
+cudaError_t launch_states_squeeze(int rate_lanes, void* lanes, uint32_t* pos, uint64_t count,
+                                  uint8_t* out, uint64_t out_len, cudaStream_t stream);
+
 // Pipe microbenchmark; see b200sha3_probe_pipe.
 cudaError_t run_pipe_probe(int mix, double* instr_per_s, double* sm_hz, cudaStream_t stream);
 

@@ -208,4 +208,78 @@ __device__ __forceinline__ void hash_message(const uint8_t* p, uint64_t len, uin
   }
 }
 
+// ---------------------------------------------------------------------------
+// Byte-granular pieces for the incremental (streaming) entry points: the state
+// carries a byte position like SpongeHasher::pos_ (sponge.hpp:60-63).
+
+// Byte mask of a 32-bit word: bytes [s, e) set, 0 <= s, e <= 4.
+__device__ __forceinline__ uint32_t byte_mask(int s, int e) {
+  if (e <= s) return 0u;
+  const uint32_t hi = e >= 4 ? 0xffffffffu : ((1u << (8 * e)) - 1u);
+  const uint32_t lo = s <= 0 ? 0u : ((1u << (8 * s)) - 1u);
+  return hi & ~lo;
+}
+
+// XORs bytes [lo, hi) of the current rate block into the state, the block being laid
+// out at the virtual pointer vp (block byte k is vp[k]; only [vp+lo, vp+hi) is message
+// data).  0 <= lo <= hi <= 8*RL.  Aligned 4-byte loads + PRMT; a word is loaded only if
+// it holds at least one byte of the range.  This is the byte loop of
+// SpongeHasher::update (sponge.cpp:100-104) for one block, done word-parallel.
+template <int RL>
+__device__ __forceinline__ void absorb_bytes(State& a, const uint8_t* vp, uint32_t lo,
+                                             uint32_t hi) {
+  const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(vp)) & 3u;
+  const uint32_t* q = reinterpret_cast<const uint32_t*>(vp - sh);
+  const uint32_t sel = 0x3210u + 0x1111u * sh;
+  // aligned word k covers block bytes [4k - sh, 4k - sh + 4)
+  auto need = [&](int k) {
+    const int first = 4 * k - static_cast<int>(sh);
+    return first < static_cast<int>(hi) && first + 4 > static_cast<int>(lo);
+  };
+  uint32_t prev = need(0) ? ld_u32(q) : 0u;
+#pragma unroll
+  for (int j = 0; j < 2 * RL; ++j) {
+    const uint32_t next = need(j + 1) ? ld_u32(q + j + 1) : 0u;
+    const uint32_t m = byte_mask(static_cast<int>(lo) - 4 * j, static_cast<int>(hi) - 4 * j);
+    const uint32_t w = __byte_perm(prev, next, sel) & m;
+    if (j & 1) {
+      a.hi[j >> 1] ^= w;
+    } else {
+      a.lo[j >> 1] ^= w;
+    }
+    prev = next;
+  }
+}
+
+// XORs `value` (one byte) into the state at byte position pos < 8*RL.
+template <int RL>
+__device__ __forceinline__ void xor_byte_at(State& a, uint32_t pos, uint32_t value) {
+  const uint32_t word = pos >> 2, shifted = value << (8u * (pos & 3u));
+#pragma unroll
+  for (int j = 0; j < 2 * RL; ++j) {
+    if (static_cast<uint32_t>(j) == word) {
+      if (j & 1) {
+        a.hi[j >> 1] ^= shifted;
+      } else {
+        a.lo[j >> 1] ^= shifted;
+      }
+    }
+  }
+}
+
+// Writes bytes [lo, hi) of the rate part to o[0 .. hi-lo) with byte stores (the general
+// form of SpongeHasher::squeeze's copy-out, sponge.cpp:135-141).
+template <int RL>
+__device__ __forceinline__ void emit_bytes(const State& a, uint8_t* o, uint32_t lo, uint32_t hi) {
+#pragma unroll
+  for (int j = 0; j < 2 * RL; ++j) {
+    const uint32_t w = state_word(a, j);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t k = 4u * j + b;
+      if (k >= lo && k < hi) o[k - lo] = static_cast<uint8_t>(w >> (8 * b));
+    }
+  }
+}
+
 }  // namespace b200sha3

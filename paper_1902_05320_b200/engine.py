@@ -25,7 +25,7 @@ ALGORITHMS = ("sha3_224", "sha3_256", "sha3_384", "sha3_512", "shake128", "shake
 _HERE = pathlib.Path(__file__).resolve().parent
 _LIB_PATH = _HERE / "libb200sha3.so"
 
-OK, ERR_INVALID_ARGUMENT, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3
+OK, ERR_INVALID_ARGUMENT, ERR_CUDA, ERR_UNSUPPORTED, ERR_STATE = 0, 1, 2, 3, 4
 FLAG_NO_BUCKETING, FLAG_NO_PIPELINE = 1, 2
 KERNEL_AUTO, KERNEL_GENERIC, KERNEL_ONEBLOCK, KERNEL_LANESPLIT = 0, 1, 2, 3
 
@@ -36,6 +36,10 @@ u64p = C.POINTER(C.c_uint64)
 
 class EngineError(RuntimeError):
     """CUDA failure or unsupported batch shape reported by the library."""
+
+
+class EngineStateError(RuntimeError):
+    """Incremental API used out of order (std::logic_error in the reference)."""
 
 
 class _Config(C.Structure):
@@ -99,6 +103,24 @@ def _load() -> C.CDLL:
     lib.b200sha3_permute_device.restype = C.c_int
     lib.b200sha3_bucket_order_device.argtypes = [C.c_int, C.c_void_p, C.c_uint64, C.c_void_p, cfgp]
     lib.b200sha3_bucket_order_device.restype = C.c_int
+    lib.b200sha3_pinned_alloc.argtypes = [C.c_uint64, C.POINTER(C.c_void_p)]
+    lib.b200sha3_pinned_alloc.restype = C.c_int
+    lib.b200sha3_pinned_free.argtypes = [C.c_void_p]
+    lib.b200sha3_pinned_free.restype = C.c_int
+    lib.b200sha3_states_create.argtypes = [C.c_int, C.c_uint64, cfgp, C.POINTER(C.c_void_p)]
+    lib.b200sha3_states_create.restype = C.c_int
+    lib.b200sha3_states_destroy.argtypes = [C.c_void_p]
+    lib.b200sha3_states_destroy.restype = C.c_int
+    lib.b200sha3_states_reset.argtypes = [C.c_void_p, cfgp]
+    lib.b200sha3_states_reset.restype = C.c_int
+    lib.b200sha3_states_update_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, cfgp]
+    lib.b200sha3_states_update_device.restype = C.c_int
+    lib.b200sha3_states_update_fixed_device.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, cfgp]
+    lib.b200sha3_states_update_fixed_device.restype = C.c_int
+    lib.b200sha3_states_finish_device.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, cfgp]
+    lib.b200sha3_states_finish_device.restype = C.c_int
+    lib.b200sha3_states_squeeze_device.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, cfgp]
+    lib.b200sha3_states_squeeze_device.restype = C.c_int
     lib.b200sha3_probe_pipe.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), cfgp]
     lib.b200sha3_probe_pipe.restype = C.c_int
     return lib
@@ -161,6 +183,8 @@ class Engine:
         if rc == ERR_INVALID_ARGUMENT:
             raise ValueError("b200sha3: invalid argument (bad algorithm id, or an XOF variant "
                              "without xof_output_bits)")
+        if rc == ERR_STATE:
+            raise EngineStateError("b200sha3: incremental API used out of order")
         detail = self.lib.b200sha3_last_cuda_error().decode()
         raise EngineError(f"b200sha3: {self.lib.b200sha3_strerror(rc).decode()}: {detail}")
 
@@ -311,6 +335,81 @@ class Engine:
         rc = self.lib.b200sha3_probe_pipe(mix, C.byref(rate), C.byref(hz), C.byref(cfg))
         self._check(rc)
         return rate.value, hz.value
+
+
+class BatchHasher:
+    """`count` incremental hashers resident in HBM -- the batch analogue of sha3::Hasher
+    (proj/core/include/sha3/sha3.hpp:66-86): update() any number of times, then digest()
+    (hash variants) or finish() + read() (XOF variants).  CUDA torch tensors in and out."""
+
+    def __init__(self, algorithm, count: int, engine: Engine | None = None):
+        self.engine = engine or Engine()
+        self.algorithm = algorithm_id(algorithm)
+        self.count = count
+        self._handle = C.c_void_p()
+        cfg, _, _ = self.engine._config(Engine._torch_stream(), False)
+        self.engine._check(self.engine.lib.b200sha3_states_create(self.algorithm, count, C.byref(cfg),
+                                                                  C.byref(self._handle)))
+
+    def close(self):
+        if self._handle:
+            self.engine.lib.b200sha3_states_destroy(self._handle)
+            self._handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _cfg(self):
+        return self.engine._config(Engine._torch_stream(), False)[0]
+
+    def update(self, data, offsets=None, lengths=None, chunk_len: int | None = None):
+        cfg = self._cfg()
+        if chunk_len is not None:
+            rc = self.engine.lib.b200sha3_states_update_fixed_device(self._handle, data.data_ptr(), chunk_len,
+                                                                     C.byref(cfg))
+        else:
+            rc = self.engine.lib.b200sha3_states_update_device(self._handle, data.data_ptr(),
+                                                               offsets.data_ptr(), lengths.data_ptr(),
+                                                               C.byref(cfg))
+        self.engine._check(rc)
+
+    def _finish(self, bits: int):
+        import torch
+        nbytes = int(self.engine.lib.b200sha3_digest_bytes(self.algorithm, bits))
+        out = torch.empty((self.count, nbytes), dtype=torch.uint8, device="cuda") if nbytes else None
+        cfg = self._cfg()
+        rc = self.engine.lib.b200sha3_states_finish_device(self._handle, bits,
+                                                           out.data_ptr() if out is not None else None,
+                                                           C.byref(cfg))
+        self.engine._check(rc)
+        return out
+
+    def digest(self):
+        """Hash variants: finalize, return (count, digest_bytes)."""
+        if self.algorithm >= 4:
+            raise EngineStateError("digest() is for fixed-output variants; use finish()/read()")
+        return self._finish(0)
+
+    def finish(self, xof_output_bits: int = 0):
+        """XOF variants: close the input; optionally return the first ceil(bits/8) bytes."""
+        if self.algorithm < 4:
+            raise EngineStateError("finish()/read() is for XOF variants; use digest()")
+        return self._finish(xof_output_bits)
+
+    def read(self, nbytes: int):
+        import torch
+        out = torch.empty((self.count, nbytes), dtype=torch.uint8, device="cuda")
+        cfg = self._cfg()
+        self.engine._check(self.engine.lib.b200sha3_states_squeeze_device(self._handle, nbytes,
+                                                                          out.data_ptr(), C.byref(cfg)))
+        return out
+
+    def reset(self):
+        cfg = self._cfg()
+        self.engine._check(self.engine.lib.b200sha3_states_reset(self._handle, C.byref(cfg)))
 
 
 def splitmix64_at(seed, n):
