@@ -212,11 +212,13 @@ __device__ __forceinline__ void hash_message(const uint8_t* p, uint64_t len, uin
 // Byte-granular pieces for the incremental (streaming) entry points: the state
 // carries a byte position like SpongeHasher::pos_ (sponge.hpp:60-63).
 
-// Byte mask of a 32-bit word: bytes [s, e) set, 0 <= s, e <= 4.
+// Byte mask of a 32-bit word: bytes [s, e) set; s and e are clamped to [0, 4].
 __device__ __forceinline__ uint32_t byte_mask(int s, int e) {
+  s = s < 0 ? 0 : (s > 4 ? 4 : s);
+  e = e < 0 ? 0 : (e > 4 ? 4 : e);
   if (e <= s) return 0u;
-  const uint32_t hi = e >= 4 ? 0xffffffffu : ((1u << (8 * e)) - 1u);
-  const uint32_t lo = s <= 0 ? 0u : ((1u << (8 * s)) - 1u);
+  const uint32_t hi = e == 4 ? 0xffffffffu : ((1u << (8 * e)) - 1u);
+  const uint32_t lo = (1u << (8 * s)) - 1u;  // s <= 3 here
   return hi & ~lo;
 }
 
