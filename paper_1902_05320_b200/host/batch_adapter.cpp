@@ -15,7 +15,7 @@ namespace sha3::b200 {
 
 namespace {
 
-unsigned resolve_workers(const EngineConfig& config) {  // batch.cpp:38-44
+unsigned pack_workers(const EngineConfig& config) {  // like resolve_workers, batch.cpp:38-44
   if (config.workers > 0) return config.workers;
   const unsigned hw = std::thread::hardware_concurrency();
   return hw > 0 ? hw : 1;
@@ -137,7 +137,7 @@ BatchResult hash_batch(const HashBatch& batch, const EngineConfig& config,
   BatchResult result;
   result.digests.resize(count);
   if (count == 0) return result;  // test_batch.cpp:113-117
-  const unsigned workers = resolve_workers(config);
+  const unsigned workers = pack_workers(config);
 
   // Pack: offsets are an 8-byte aligned running sum so the device can use
   // aligned 64-bit loads; equal lengths that are a multiple of 8 need no

@@ -32,3 +32,22 @@ def test_adapter_all_cases():
     out = subprocess.run([str(EXE)], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 failures" in out.stdout
+
+
+@pytest.mark.gpu
+def test_reference_runner_on_our_backend():
+    """Binding 2 of INTEGRATION.md, executed: the reference's unmodified run_benchmark /
+    emit_csv / generate_workload, linked against our sha3::hash_batch instead of its
+    batch.cpp (tests/integration/, built where /root/reference is mounted).  The binary also
+    cross-checks 5000 digests against the reference's own CPU sha3_digest."""
+    exe = ROOT / "tests" / "integration" / "_build" / "ref_runner_on_b200"
+    subprocess.run(["make", "-C", str(ROOT / "tests" / "integration")], check=False,
+                   stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    if not exe.exists():
+        pytest.skip("integration binary not built (needs /root/reference at build time)")
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    lines = out.stdout.strip().splitlines()
+    assert lines[0] == "total_bytes,message_size,message_count,backend,time_seconds,throughput_bps,repeats"
+    assert len(lines) == 5 and lines[1].startswith("64000,64,1000,")
+    assert "5000/5000 digests equal" in lines[-1]
