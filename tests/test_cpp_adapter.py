@@ -38,10 +38,11 @@ def test_adapter_all_cases():
 def test_reference_runner_on_our_backend():
     """Binding 2 of INTEGRATION.md, executed: the reference's unmodified run_benchmark /
     emit_csv / generate_workload, linked against our sha3::hash_batch instead of its
-    batch.cpp (tests/integration/, built where /root/reference is mounted).  The binary also
+    batch.cpp (recipe: oracle/Makefile `runner`; source: tests/integration/ref_runner_main.cpp;
+    built where /root/reference is mounted).  The binary also
     cross-checks 5000 digests against the reference's own CPU sha3_digest."""
-    exe = ROOT / "tests" / "integration" / "_build" / "ref_runner_on_b200"
-    subprocess.run(["make", "-C", str(ROOT / "tests" / "integration")], check=False,
+    exe = ROOT / "oracle" / "_ref" / "ref_runner_on_b200"
+    subprocess.run(["make", "-C", str(ROOT / "oracle"), "runner"], check=False,
                    stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
     if not exe.exists():
         pytest.skip("integration binary not built (needs /root/reference at build time)")
