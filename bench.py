@@ -294,10 +294,20 @@ def main():
         torch.cuda.synchronize()
         e2e_seconds = max_over_ranks(time.perf_counter() - t0)
         same = bool(torch.equal(host_out.view(count, DIGEST_BYTES)[:4096], digests[:4096].cpu()))
+        # what bounds e2e: the PCIe link.  A plain pinned H2D copy of the same buffer, alone
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        data.copy_(host_in, non_blocking=True)
+        torch.cuda.synchronize()
+        plain_h2d_gbs = count * MSG_LEN / (time.perf_counter() - t0) / 1e9
         e2e = {"value": total * e2e_steps / e2e_seconds, "unit": "hashes/s",
                "h2d_bytes_per_step": total * MSG_LEN, "d2h_bytes_per_step": total * DIGEST_BYTES,
                "steps": e2e_steps, "ms_per_step": e2e_seconds / e2e_steps * 1e3,
                "digests_match_device_path": same,
+               "pcie": {"h2d_gb_per_s_inside_pipeline": count * MSG_LEN * e2e_steps / e2e_seconds / 1e9,
+                        "d2h_gb_per_s_inside_pipeline": count * DIGEST_BYTES * e2e_steps / e2e_seconds / 1e9,
+                        "h2d_gb_per_s_plain_pinned_copy": plain_h2d_gbs,
+                        "note": "per rank; e2e is bound by the host link, not by the kernel"},
                "note": "b200sha3_hash_fixed on pinned host buffers: chunked H2D / kernel / D2H "
                        "pipeline inside the call; wall clock, max over ranks"}
         del host_in, host_out

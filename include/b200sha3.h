@@ -135,6 +135,9 @@ B200SHA3_API const char* b200sha3_last_cuda_error(void);
 
 B200SHA3_API const char* b200sha3_version(void);
 
+/* Number of CUDA devices visible to the process (0 if CUDA is unusable). */
+B200SHA3_API int b200sha3_device_count(void);
+
 /* ---- host-buffer entries (the hash_batch drop-in) ------------------------
  * All pointers are HOST pointers.  The call copies the batch to the device
  * (chunked and overlapped with compute when the host memory is pinned), hashes

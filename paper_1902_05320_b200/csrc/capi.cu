@@ -204,6 +204,15 @@ const char* b200sha3_last_cuda_error(void) { return last_error_buffer(); }
 
 const char* b200sha3_version(void) { return "b200sha3 0.1 (sm_100a)"; }
 
+int b200sha3_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
 int b200sha3_hash_fixed_device(int algorithm, const uint8_t* d_data, uint64_t msg_len,
                                uint64_t count, uint64_t xof_output_bits, uint8_t* d_digests,
                                const b200sha3_config* cfg) {

@@ -108,6 +108,13 @@ b200sha3_config make_config(const DeviceConfig& device, double* ms) {
 
 }  // namespace
 
+DeviceConfig DeviceConfig::all_devices() {
+  DeviceConfig cfg;
+  const int n = b200sha3_device_count();
+  for (int d = 0; d < n; ++d) cfg.devices.push_back(d);
+  return cfg;
+}
+
 std::vector<std::uint8_t> hash_packed(Algorithm algorithm, const std::uint8_t* data,
                                       const std::uint64_t* offsets,
                                       const std::uint64_t* lengths, std::uint64_t count,
@@ -163,11 +170,61 @@ BatchResult hash_batch(const HashBatch& batch, const EngineConfig& config,
 
   std::uint8_t* packed = t_digest_staging.reserve(std::max<std::uint64_t>(count * digest_bytes, 16));
   double ms = 0.0;
-  b200sha3_config cfg = make_config(device, &ms);
-  const int rc =
-      fixed ? b200sha3_hash_fixed(alg, data, first_len, count, batch.xof_output_bits, packed, &cfg)
-            : b200sha3_hash_batch(alg, data, offsets.data(), lengths.data(), count,
-                                  batch.xof_output_bits, packed, &cfg);
+  int rc = B200SHA3_OK;
+  if (device.devices.size() <= 1) {
+    b200sha3_config cfg = make_config(device, &ms);
+    if (device.devices.size() == 1) cfg.device = device.devices[0];
+    rc = fixed ? b200sha3_hash_fixed(alg, data, first_len, count, batch.xof_output_bits, packed, &cfg)
+               : b200sha3_hash_batch(alg, data, offsets.data(), lengths.data(), count,
+                                     batch.xof_output_bits, packed, &cfg);
+  } else {
+    // One contiguous range per device, cut at equal cumulative permutation counts.
+    const std::size_t ndev = device.devices.size();
+    const std::uint64_t rate = b200sha3_rate_bytes(alg);
+    std::uint64_t work = 0;
+    for (std::size_t i = 0; i < count; ++i) work += lengths[i] / rate + 1;
+    std::vector<std::size_t> cut(ndev + 1, count);
+    cut[0] = 0;
+    std::uint64_t acc = 0;
+    std::size_t next = 1;
+    for (std::size_t i = 0; i < count && next < ndev; ++i) {
+      while (next < ndev && acc >= work * next / ndev) cut[next++] = i;
+      acc += lengths[i] / rate + 1;
+    }
+    std::vector<int> status(ndev, B200SHA3_OK);
+    std::vector<double> dev_ms(ndev, 0.0);
+    std::vector<std::string> errors(ndev);
+    auto run = [&](std::size_t k) {
+      const std::size_t b = cut[k], e = cut[k + 1];
+      if (e <= b) return;
+      b200sha3_config cfg = make_config(device, &dev_ms[k]);
+      cfg.device = device.devices[k];
+      cfg.stream = nullptr;
+      status[k] = fixed ? b200sha3_hash_fixed(alg, data + b * first_len, first_len, e - b,
+                                              batch.xof_output_bits, packed + b * digest_bytes, &cfg)
+                        : b200sha3_hash_batch(alg, data, offsets.data() + b, lengths.data() + b, e - b,
+                                              batch.xof_output_bits, packed + b * digest_bytes, &cfg);
+      if (status[k] != B200SHA3_OK) errors[k] = b200sha3_last_cuda_error();  // thread-local text
+    };
+    {
+      std::vector<std::thread> pool;
+      for (std::size_t k = 1; k < ndev; ++k) pool.emplace_back(run, k);
+      run(0);  // the caller drives the first device (batch.cpp:126)
+      for (auto& t : pool) t.join();
+    }
+    for (std::size_t k = 0; k < ndev; ++k) {
+      ms = std::max(ms, dev_ms[k]);
+      if (status[k] != B200SHA3_OK && rc == B200SHA3_OK) {  // first failure wins (batch.cpp:111-117)
+        rc = status[k];
+        if (rc != B200SHA3_ERR_INVALID_ARGUMENT) {
+          t_data_staging.trim(0);
+          t_digest_staging.trim(0);
+          throw DeviceError(rc, std::string("b200sha3: ") + b200sha3_strerror(rc) + " on device " +
+                                    std::to_string(device.devices[k]) + ": " + errors[k]);
+        }
+      }
+    }
+  }
   if (rc != B200SHA3_OK) {
     t_data_staging.trim(0);
     t_digest_staging.trim(0);

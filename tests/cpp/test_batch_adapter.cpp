@@ -223,6 +223,37 @@ void gpu_cases() {
     }
     CHECK(ok);
   }
+  {  // several devices: contiguous ranges of equal work, one host thread each.  The box has
+     // one GPU, so the same ordinal is listed three times -- the sharding, threading and
+     // in-order digest placement are what is under test.
+    Rng rng(91);
+    HashBatch batch = random_batch(rng, 5000, 700);
+    b200::DeviceConfig dev;
+    dev.devices = {0, 0, 0};
+    for (int a : {1, 4}) {
+      batch.algorithm = static_cast<Algorithm>(a);
+      batch.xof_output_bits = a >= 4 ? 1352 : 0;
+      CHECK(matches_oracle(batch, b200::hash_batch(batch, {}, dev)));
+    }
+    HashBatch fixed_batch;
+    fixed_batch.messages.assign(10007, std::vector<std::uint8_t>(64, 0));
+    for (std::size_t i = 0; i < fixed_batch.messages.size(); ++i) {
+      fixed_batch.messages[i][i % 64] = static_cast<std::uint8_t>(i);
+    }
+    CHECK(matches_oracle(fixed_batch, b200::hash_batch(fixed_batch, {}, dev)));
+    HashBatch tiny;
+    tiny.messages = {{1, 2, 3}};
+    CHECK(matches_oracle(tiny, b200::hash_batch(tiny, {}, dev)));   // fewer messages than devices
+    CHECK(b200::DeviceConfig::all_devices().devices.size() >= 1);
+    dev.devices = {0, 99};                                          // a device that does not exist
+    bool threw = false;
+    try {
+      b200::hash_batch(batch, {}, dev);
+    } catch (const b200::DeviceError& e) {
+      threw = std::string(e.what()).find("device 99") != std::string::npos;
+    }
+    CHECK(threw);
+  }
   {  // hash_packed on caller-packed buffers with odd offsets
     const std::vector<std::uint8_t> data = {9, 9, 9, 'a', 'b', 'c', 7, 7, 1, 2, 3, 4, 5};
     const std::uint64_t offsets[] = {3, 8, 0}, lengths[] = {3, 5, 0};
