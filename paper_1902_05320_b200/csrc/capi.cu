@@ -52,11 +52,12 @@ int validate(int algorithm, uint64_t xof_bits, uint64_t* digest_bytes) {
   return B200SHA3_OK;
 }
 
-// Equal-length batch already in HBM, on the current device.  `launches` counts
-// kernels.  Asynchronous on `stream`.
-int run_fixed_device(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint64_t count,
-                     uint64_t xof_bits, uint64_t digest_bytes, uint8_t* d_digests,
-                     const Config& c, cudaStream_t stream, uint32_t* launches) {
+namespace {
+
+// One launch: at most 2^30 equal-length messages.
+int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint64_t count,
+                    uint64_t xof_bits, uint64_t digest_bytes, uint8_t* d_digests,
+                    const Config& c, cudaStream_t stream, uint32_t* launches) {
   const Variant& v = kVariants[algorithm];
   HashArgs args{};
   args.data = d_data;
@@ -106,6 +107,24 @@ int run_fixed_device(int algorithm, const uint8_t* d_data, uint64_t msg_len, uin
   }
   if (err != cudaSuccess) return cuda_fail(err, "hash kernel launch");
   if (launches) *launches += 1;
+  return B200SHA3_OK;
+}
+
+}  // namespace
+
+// Equal-length batch already in HBM, on the current device; one launch per slice of 2^30
+// messages (the grid is 32-bit).  `launches` counts kernels.  Asynchronous on `stream`.
+int run_fixed_device(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint64_t count,
+                     uint64_t xof_bits, uint64_t digest_bytes, uint8_t* d_digests,
+                     const Config& c, cudaStream_t stream, uint32_t* launches) {
+  constexpr uint64_t kSlice = 1ull << 30;
+  for (uint64_t first = 0; first < count; first += kSlice) {
+    const uint64_t n = std::min<uint64_t>(kSlice, count - first);
+    if (int rc = run_fixed_slice(algorithm, d_data + first * msg_len, msg_len, n, xof_bits,
+                                 digest_bytes, d_digests + first * digest_bytes, c, stream, launches)) {
+      return rc;
+    }
+  }
   return B200SHA3_OK;
 }
 

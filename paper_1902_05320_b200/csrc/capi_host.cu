@@ -2,6 +2,7 @@
 // chunked copy / compute pipelines over the device paths of capi.cu, and the pinned
 // staging allocator.
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -19,6 +20,17 @@ using namespace b200sha3::capi;
 // copy of chunk k-1 overlap.  Anything else takes one copy of the byte range the batch
 // touches, one device pass, one copy back.
 namespace {
+
+// Pipeline chunk size (bytes of input + output per chunk).  64 MiB measured best on the
+// B200 boxes; B200SHA3_CHUNK_MIB overrides it for experiments.
+uint64_t chunk_target_bytes() {
+  static const uint64_t value = [] {
+    const char* env = std::getenv("B200SHA3_CHUNK_MIB");
+    const long mib = env ? std::atol(env) : 0;
+    return static_cast<uint64_t>(mib > 0 ? mib : 64) << 20;
+  }();
+  return value;
+}
 
 struct HostChunk {
   uint64_t first, count;  // message range
@@ -228,7 +240,7 @@ int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_t msg_len, ui
   constexpr int kSlots = 3;
   const bool pipeline = (c.flags & B200SHA3_FLAG_NO_PIPELINE) == 0;
   const uint64_t per_msg = std::max<uint64_t>(1, msg_len + digest_bytes);
-  uint64_t chunk = pipeline ? std::max<uint64_t>(1, (64ull << 20) / per_msg) : count;
+  uint64_t chunk = pipeline ? std::max<uint64_t>(1, chunk_target_bytes() / per_msg) : count;
   chunk = std::min(chunk, count);
   // keep every chunk start 16-byte aligned in both buffers
   if (chunk < count) chunk = std::max<uint64_t>(16, chunk & ~15ull);
@@ -321,7 +333,7 @@ int b200sha3_hash_batch(int algorithm, const uint8_t* data, const uint64_t* offs
   if (c.stream) CU(cudaStreamSynchronize(c.stream));
   std::vector<HostChunk> chunks;
   const bool pipeline = (c.flags & B200SHA3_FLAG_NO_PIPELINE) == 0 && data != nullptr &&
-                        plan_host_chunks(offsets, lengths, count, 64ull << 20, &chunks) &&
+                        plan_host_chunks(offsets, lengths, count, chunk_target_bytes(), &chunks) &&
                         chunks.size() > 1;
   if (pipeline) {
     return hash_batch_host_pipelined(algorithm, data, offsets, lengths, xof_output_bits,
