@@ -23,6 +23,43 @@ namespace {
 
 // Pipeline chunk size (bytes of input + output per chunk).  64 MiB measured best on the
 // B200 boxes; B200SHA3_CHUNK_MIB overrides it for experiments.
+// Streams of the copy/compute pipeline, created once per (calling thread, device) and
+// reused: creating and destroying three streams per call costs more than hashing a small
+// batch.  A thread's streams are only ever used by that thread, so calls stay reentrant.
+constexpr int kPipelineSlots = 3;
+
+class StreamCache {
+ public:
+  cudaError_t get(int slot, cudaStream_t* out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= static_cast<int>(per_device_.size())) per_device_.resize(dev + 1);
+    cudaStream_t& s = per_device_[dev].streams[slot];
+    if (!s) {
+      e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+    }
+    *out = s;
+    return cudaSuccess;
+  }
+  ~StreamCache() {
+    for (auto& d : per_device_) {
+      for (cudaStream_t s : d.streams) {
+        if (s) cudaStreamDestroy(s);  // harmless error if the context is already gone
+      }
+    }
+  }
+
+ private:
+  struct Entry {
+    cudaStream_t streams[kPipelineSlots] = {};
+  };
+  std::vector<Entry> per_device_;
+};
+
+thread_local StreamCache t_streams;
+
 uint64_t chunk_target_bytes() {
   static const uint64_t value = [] {
     const char* env = std::getenv("B200SHA3_CHUNK_MIB");
@@ -76,7 +113,7 @@ int hash_batch_host_single(int algorithm, const uint8_t* data, const uint64_t* o
   if (hi > lo && !data) return B200SHA3_ERR_INVALID_ARGUMENT;
   lo &= ~15ull;  // keep the device copy congruent to the host buffer modulo 16
   cudaStream_t s = nullptr;
-  CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  CU(t_streams.get(0, &s));
   uint8_t* d_data = nullptr;
   uint64_t* d_meta = nullptr;
   uint8_t* d_out = nullptr;
@@ -121,7 +158,6 @@ int hash_batch_host_single(int algorithm, const uint8_t* data, const uint64_t* o
   cudaStreamSynchronize(s);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
-  cudaStreamDestroy(s);
   if (rc != B200SHA3_OK) {
     cudaGetLastError();
     return rc;
@@ -134,7 +170,7 @@ int hash_batch_host_pipelined(int algorithm, const uint8_t* data, const uint64_t
                               const uint64_t* lengths, uint64_t xof_output_bits,
                               uint64_t digest_bytes, uint8_t* digests, const Config& c,
                               const std::vector<HostChunk>& chunks) {
-  constexpr int kSlots = 3;
+  constexpr int kSlots = kPipelineSlots;
   uint64_t max_span = 16, max_count = 1;
   for (const HostChunk& ch : chunks) {
     max_span = std::max(max_span, ch.hi - ch.lo);
@@ -148,7 +184,7 @@ int hash_batch_host_pipelined(int algorithm, const uint8_t* data, const uint64_t
   cudaEvent_t ev0[kSlots] = {}, ev1[kSlots] = {};
   int rc = B200SHA3_OK;
   for (int s = 0; s < slots && rc == B200SHA3_OK; ++s) {
-    cudaError_t e = cudaStreamCreateWithFlags(&streams[s], cudaStreamNonBlocking);
+    cudaError_t e = t_streams.get(s, &streams[s]);
     if (e == cudaSuccess) e = cudaMallocAsync(&d_data[s], max_span, streams[s]);
     if (e == cudaSuccess) e = cudaMallocAsync(&d_meta[s], 2 * max_count * sizeof(uint64_t), streams[s]);
     if (e == cudaSuccess) e = cudaMallocAsync(&d_out[s], max_count * digest_bytes, streams[s]);
@@ -203,7 +239,6 @@ int hash_batch_host_pipelined(int algorithm, const uint8_t* data, const uint64_t
     cudaStreamSynchronize(streams[s]);
     if (ev0[s]) cudaEventDestroy(ev0[s]);
     if (ev1[s]) cudaEventDestroy(ev1[s]);
-    cudaStreamDestroy(streams[s]);
   }
   if (rc != B200SHA3_OK) {
     cudaGetLastError();
@@ -237,7 +272,7 @@ int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_t msg_len, ui
   tune_mempool_once();
   if (c.stream) CU(cudaStreamSynchronize(c.stream));
 
-  constexpr int kSlots = 3;
+  constexpr int kSlots = kPipelineSlots;
   const bool pipeline = (c.flags & B200SHA3_FLAG_NO_PIPELINE) == 0;
   const uint64_t per_msg = std::max<uint64_t>(1, msg_len + digest_bytes);
   uint64_t chunk = pipeline ? std::max<uint64_t>(1, chunk_target_bytes() / per_msg) : count;
@@ -254,7 +289,7 @@ int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_t msg_len, ui
   int rc = B200SHA3_OK;
   auto fail = [&](cudaError_t e, const char* what) { rc = cuda_fail(e, what); };
   for (int s = 0; s < slots && rc == B200SHA3_OK; ++s) {
-    cudaError_t e = cudaStreamCreateWithFlags(&streams[s], cudaStreamNonBlocking);
+    cudaError_t e = t_streams.get(s, &streams[s]);
     if (e == cudaSuccess) e = cudaMallocAsync(&d_in[s], std::max<uint64_t>(16, chunk * msg_len), streams[s]);
     if (e == cudaSuccess) e = cudaMallocAsync(&d_out[s], chunk * digest_bytes, streams[s]);
     if (e == cudaSuccess && c.device_ms) {
@@ -306,7 +341,6 @@ int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_t msg_len, ui
     cudaStreamSynchronize(streams[s]);
     if (ev0[s]) cudaEventDestroy(ev0[s]);
     if (ev1[s]) cudaEventDestroy(ev1[s]);
-    cudaStreamDestroy(streams[s]);
   }
   if (rc != B200SHA3_OK) {
     cudaGetLastError();
