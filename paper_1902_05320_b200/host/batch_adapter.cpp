@@ -146,21 +146,21 @@ BatchResult hash_batch(const HashBatch& batch, const EngineConfig& config,
   if (count == 0) return result;  // test_batch.cpp:113-117
   const unsigned workers = pack_workers(config);
 
-  // Pack: offsets are an 8-byte aligned running sum so the device can use
-  // aligned 64-bit loads; equal lengths that are a multiple of 8 need no
-  // offset table at all (the fixed-length entry).
+  // Pack.  Equal-length batches (what generate_workload builds, workload.cpp:34-45) go back
+  // to back and take the fixed-length entry: no offset table, no bucketing pass, one launch.
+  // Ragged batches get 8-byte aligned offsets so the device can use aligned 64-bit loads.
   std::vector<std::uint64_t> offsets(count), lengths(count);
-  std::uint64_t total = 0;
-  bool fixed = true;
   const std::uint64_t first_len = batch.messages[0].size();
+  bool fixed = true;
   for (std::size_t i = 0; i < count; ++i) {
-    const std::uint64_t len = batch.messages[i].size();
-    offsets[i] = total;
-    lengths[i] = len;
-    fixed = fixed && len == first_len;
-    total += (len + 7) & ~std::uint64_t{7};
+    lengths[i] = batch.messages[i].size();
+    fixed = fixed && lengths[i] == first_len;
   }
-  fixed = fixed && (first_len % 8 == 0 || count == 1);
+  std::uint64_t total = 0;
+  for (std::size_t i = 0; i < count; ++i) {
+    offsets[i] = total;
+    total += fixed ? first_len : ((lengths[i] + 7) & ~std::uint64_t{7});
+  }
   std::uint8_t* data = t_data_staging.reserve(std::max<std::uint64_t>(total, 16));
   parallel_ranges(count, workers, total, [&](std::size_t begin, std::size_t end) {
     for (std::size_t i = begin; i < end; ++i) {
