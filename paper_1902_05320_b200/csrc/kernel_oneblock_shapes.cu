@@ -13,8 +13,8 @@ namespace b200sha3 {
   X(13, 4, 12) X(13, 8, 12)                /* SHA3-384: 32/64 B -> 48 B      */ \
   X(9, 4, 16) X(9, 8, 16)                  /* SHA3-512: 32/64 B -> 64 B      */ \
   X(21, 4, 8) X(21, 8, 8) X(21, 16, 8)     /* SHAKE128 -> 256 bits           */ \
-  X(21, 8, 16)                             /* SHAKE128 64 B -> 512 bits      */ \
-  X(17, 8, 16)                             /* SHAKE256 64 B -> 512 bits      */
+  X(21, 8, 16) X(21, 8, 32)                /* SHAKE128 64 B -> 512 / 1024 bits */ \
+  X(17, 8, 16) X(17, 8, 32)                /* SHAKE256 64 B -> 512 / 1024 bits */
 
 bool oneblock_shape_exists(int rl, int ml, int ow) {
   if (rl == 17 && ml == 8 && ow == 8) return true;  // the tuning-matrix shape

@@ -204,7 +204,7 @@ def test_every_kernel_variant_agrees(engine, oracle):
 @pytest.mark.parametrize("algorithm,msg_len,bits", [
     (0, 32, 0), (0, 64, 0), (0, 128, 0), (1, 32, 0), (1, 64, 0), (1, 128, 0), (2, 32, 0), (2, 64, 0),
     (3, 32, 0), (3, 64, 0), (4, 32, 256), (4, 64, 256), (4, 128, 256), (4, 64, 512), (5, 64, 256),
-    (5, 64, 512), (5, 32, 256), (5, 128, 256)])
+    (5, 64, 512), (5, 32, 256), (5, 128, 256), (4, 64, 1024), (5, 64, 1024)])
 def test_oneblock_shapes(oracle, algorithm, msg_len, bits):
     """Every instantiated shape of the single-block kernel, forced, vs the oracle; shapes
     without an instantiation must be refused (no silent substitution)."""
