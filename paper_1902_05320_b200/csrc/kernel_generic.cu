@@ -4,7 +4,7 @@
 // Replaces the per-message body of hash_batch's fan-out
 // (proj/core/src/batch.cpp:86-109 -> hash_into :15-25) for arbitrary batches.
 // Threads of a warp run the same instruction stream; they diverge only in the
-// number of blocks, which the bucketing pass (bucket.cu) bounds.
+// number of blocks, which the bucketing pass (kernel_aux.cu) bounds.
 #include "kernels.cuh"
 #include "sponge.cuh"
 
@@ -40,8 +40,9 @@ cudaError_t launch_one(const HashArgs& args, const LaunchPlan& plan, cudaStream_
 
 template <int RL>
 cudaError_t launch_rl(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {
-  // Generic kernel instantiations: rolled loop (2 rounds per body), ALU-only or
-  // the measured-best FMA preset.
+  // Generic kernel instantiations: rolled loop (2 rounds per body); ALU only (the
+  // default) or FMA preset 5 (every rho rotation on the FMA pipe), kept for the measured
+  // comparison of DESIGN.md section 4.
   switch (plan.fma_preset) {
     case 0: return launch_one<RL, 2, 0>(args, plan, stream);
     default: return launch_one<RL, 2, 5>(args, plan, stream);
