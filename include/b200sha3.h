@@ -89,8 +89,11 @@ enum {
   B200SHA3_KERNEL_AUTO = 0,
   B200SHA3_KERNEL_GENERIC = 1,   /* rolled rounds, any length / alignment        */
   B200SHA3_KERNEL_ONEBLOCK = 2,  /* specialised single-block kernel when it fits  */
-  B200SHA3_KERNEL_LANESPLIT = 3  /* 5 threads per state + warp shuffles (kept for
+  B200SHA3_KERNEL_LANESPLIT = 3, /* 5 threads per state + warp shuffles (kept for
                                     the measured comparison in DESIGN.md)         */
+  B200SHA3_KERNEL_STAGED = 4     /* generic kernel with rate blocks staged through
+                                    shared memory by bulk async copies (TMA); also
+                                    kept for the measured comparison               */
 };
 
 /* Optional per-call configuration; NULL means all defaults.  The analogue of

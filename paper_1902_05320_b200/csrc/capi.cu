@@ -95,6 +95,8 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
       return B200SHA3_ERR_UNSUPPORTED;
     }
     err = launch_hash_lanesplit(args, plan, stream);
+  } else if (kernel == B200SHA3_KERNEL_STAGED) {
+    err = launch_hash_staged(args, plan, stream);
   } else {
     plan.unroll = 2;
     plan.fma_preset = c.fma_preset >= 0 ? c.fma_preset : kDefaultFmaGeneric;
@@ -172,7 +174,8 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     plan.unroll = 2;
     plan.fma_preset = c.fma_preset >= 0 ? c.fma_preset : kDefaultFmaGeneric;
     plan.block_threads = c.block_threads;
-    cudaError_t err = launch_hash_generic(args, plan, stream);
+    cudaError_t err = c.kernel == B200SHA3_KERNEL_STAGED ? launch_hash_staged(args, plan, stream)
+                                                         : launch_hash_generic(args, plan, stream);
     if (err != cudaSuccess) {
       cudaFreeAsync(scratch, stream);
       return cuda_fail(err, "hash kernel launch");

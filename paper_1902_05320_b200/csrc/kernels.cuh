@@ -67,6 +67,10 @@ cudaError_t launch_hash_lanesplit(const HashArgs& args, const LaunchPlan& plan,
                                   cudaStream_t stream);
 bool lanesplit_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
 
+// TMA-staged variant of the generic kernel (kernel_staged.cu); blocks are staged when the
+// data base is 16-byte aligned and message starts are 8-byte aligned (else direct loads).
+cudaError_t launch_hash_staged(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
+
 // Keccak-f[1600] on raw 200-byte states (test hook).
 cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream);
 

@@ -237,6 +237,32 @@ def test_lanesplit_kernel(oracle, algorithm, msg_len, bits):
         assert (got.cpu().numpy() == expect).all(), count
 
 
+@pytest.mark.parametrize("algorithm", range(6))
+def test_staged_kernel(oracle, algorithm):
+    """The TMA-staged comparison kernel (bulk async copies into shared memory, mbarrier
+    completion): ragged batch with many multi-block messages at 8-byte aligned offsets, the
+    same batch at odd offsets (nothing staged, direct path), and a fixed-length batch."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import KERNEL_STAGED
+    rng = np.random.default_rng(70 + algorithm)
+    rate = oracle.rate_bytes(algorithm)
+    bits = 0 if algorithm < 4 else 8 * rate + 40
+    lens = list(rng.integers(0, 12 * rate, 900)) + [rate + 15, rate + 16, rate + 17, 2 * rate + 16, 3 * rate,
+                                                     5 * rate + 8, 40 * rate + 3]
+    msgs = [rng.integers(0, 256, int(n), dtype=np.uint8).tobytes() for n in lens]
+    expect = [oracle.hash_one(algorithm, m, bits) for m in msgs]
+    eng = Engine(kernel=KERNEL_STAGED)
+    for align, lead in ((8, 0), (16, 0), (8, 8), (1, 0), (8, 3)):
+        got = device_digests(eng, algorithm, msgs, bits, align, lead)
+        assert [g.tobytes() for g in got] == expect, (align, lead)
+    count, msg_len = 3001, 4 * rate + 8
+    host = oracle.generate_workload(count * msg_len, msg_len, seed=41)
+    dev = torch.from_numpy(host).cuda()
+    want = oracle.hash_batch(algorithm, host, fixed_len=msg_len, count=count, xof_bits=bits, workers=4)
+    assert (eng.hash_fixed(algorithm, dev, msg_len, count, bits).cpu().numpy() == want).all()
+
+
 def test_bucket_order_is_a_sorted_permutation(engine):
     """Device bucketing: every index exactly once, block counts non-increasing
     up to the bin width."""

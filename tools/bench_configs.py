@@ -83,7 +83,9 @@ def main():
         out = torch.empty((count, 32), dtype=torch.uint8, device="cuda")
         msg_bytes = int(lengths.sum().item())
         perms = int((lengths // 136 + 1).sum().item())
-        for label, eng in (("bucketed", e), ("input order (no bucketing)", Engine(flags=FLAG_NO_BUCKETING))):
+        from paper_1902_05320_b200.engine import KERNEL_STAGED
+        for label, eng in (("bucketed", e), ("input order (no bucketing)", Engine(flags=FLAG_NO_BUCKETING)),
+                           ("bucketed, TMA-staged kernel", Engine(kernel=KERNEL_STAGED))):
             def run():
                 eng.hash_batch("sha3_256", data, offsets, lengths, out=out, timed=True)
                 return eng.last_device_ms
