@@ -101,3 +101,40 @@ def test_two_rank_gloo_run_matches_single_rank(oracle):
         check ^= checksum
     assert check == xor_fold_checksum(whole)
     assert [g[:2] for g in gathered] == [shard_range(total, r, world) for r in range(world)]
+
+
+def test_shard_properties_hypothesis():
+    """Property form of the partition tests of proj/tests/test_batch.cpp:51-70: ranges are
+    contiguous, disjoint and cover the batch, for any batch shape and GPU count."""
+    from hypothesis import given, settings, strategies as st
+
+    @settings(max_examples=200, deadline=None)
+    @given(st.integers(0, 10**12), st.integers(1, 16))
+    def fixed(total, world):
+        pos = 0
+        sizes = []
+        for rank in range(world):
+            first, count = shard_range(total, rank, world)
+            assert first == pos and count >= 0
+            pos += count
+            sizes.append(count)
+        assert pos == total and max(sizes) - min(sizes) <= 1
+
+    @settings(max_examples=100, deadline=None)
+    @given(st.lists(st.integers(0, 20000), min_size=0, max_size=300), st.integers(1, 8),
+           st.sampled_from([72, 104, 136, 144, 168]))
+    def ragged(lengths, world, rate):
+        ranges = shard_ranges_by_blocks(np.array(lengths, dtype=np.uint64), rate, world)
+        assert len(ranges) == world
+        pos = 0
+        for first, count in ranges:
+            assert first == pos and count >= 0
+            pos += count
+        assert pos == len(lengths)
+        if lengths:
+            blocks = np.array(lengths) // rate + 1
+            work = [int(blocks[f:f + c].sum()) for f, c in ranges]
+            assert max(work) <= int(blocks.sum()) / world + int(blocks.max()) + 1
+
+    fixed()
+    ragged()
