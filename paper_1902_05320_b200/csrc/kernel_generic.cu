@@ -13,7 +13,7 @@ namespace b200sha3 {
 namespace {
 
 template <int RL, int UNROLL, uint32_t FMA_MASK>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 hash_generic_kernel(const HashArgs args) {
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (tid >= args.count) return;

@@ -73,13 +73,15 @@ __device__ __forceinline__ void absorb_tail(State& a, const uint8_t* p, uint32_t
     absorb_lanes_aligned<RL>(a, p, fl);
     const uint8_t* tp = p + 8u * fl;
     uint32_t tlo = 0u, thi = 0u;
+    if (rb != 0u) {  // whole-lane messages (the common case) skip the byte loads
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      if (static_cast<uint32_t>(b) < rb) tlo |= ld_u8(tp + b) << (8 * b);
-    }
+      for (int b = 0; b < 4; ++b) {
+        if (static_cast<uint32_t>(b) < rb) tlo |= ld_u8(tp + b) << (8 * b);
+      }
 #pragma unroll
-    for (int b = 4; b < 7; ++b) {
-      if (static_cast<uint32_t>(b) < rb) thi |= ld_u8(tp + b) << (8 * (b - 4));
+      for (int b = 4; b < 7; ++b) {
+        if (static_cast<uint32_t>(b) < rb) thi |= ld_u8(tp + b) << (8 * (b - 4));
+      }
     }
     if (rb < 4u) {
       tlo |= head << (8u * rb);
@@ -170,8 +172,11 @@ __device__ __forceinline__ void emit_block(const State& a, uint8_t* o, uint32_t 
 //   head         0x06 (SHA-3) or 0x1f (SHAKE)
 //   last_mask    0xff, or (1 << bits%8) - 1 for an XOF length that is not a
 //                multiple of 8 (batch.cpp:22-24)
-// The permutation is instantiated once: absorb blocks and squeeze blocks share
-// one loop.
+// Three phases, each with its own copy of the (rolled) permutation so that the hot
+// full-block loop carries nothing but loads, XORs and the rounds:
+//   absorb   floor(len/R) whole blocks                      (sponge.cpp:81-111)
+//   finish   the partial block + pad, one permutation       (sponge.cpp:113-129)
+//   squeeze  out_len bytes, a permutation between blocks    (sponge.cpp:131-143)
 template <int RL, int UNROLL, uint32_t FMA_MASK>
 __device__ __forceinline__ void hash_message(const uint8_t* p, uint64_t len, uint8_t* out,
                                              uint64_t out_len, uint32_t head,
@@ -179,29 +184,33 @@ __device__ __forceinline__ void hash_message(const uint8_t* p, uint64_t len, uin
   constexpr uint32_t R = 8u * RL;
   State a;
   state_zero(a);
-  const uint64_t nfull = len / R;
-  const uint32_t rem = static_cast<uint32_t>(len - nfull * R);
-  const uint64_t iters = nfull + 1u + (out_len - 1u) / R;
+  uint64_t left_in = len;
+  if (aligned8) {
+    while (left_in >= R) {
+      absorb_lanes_aligned<RL>(a, p, RL);
+      keccak_f1600<UNROLL, FMA_MASK>(a);
+      p += R;
+      left_in -= R;
+    }
+  } else {
+    while (left_in >= R) {
+      absorb_words_unaligned<RL>(a, p, 2 * RL);
+      keccak_f1600<UNROLL, FMA_MASK>(a);
+      p += R;
+      left_in -= R;
+    }
+  }
+  absorb_tail<RL>(a, p, static_cast<uint32_t>(left_in), head, aligned8);
+  keccak_f1600<UNROLL, FMA_MASK>(a);
   uint8_t* o = out;
   uint64_t left = out_len;
-  for (uint64_t it = 0; it < iters; ++it) {
-    if (it < nfull) {
-      if (aligned8) {
-        absorb_lanes_aligned<RL>(a, p, RL);
-      } else {
-        absorb_words_unaligned<RL>(a, p, 2 * RL);
-      }
-      p += R;
-    } else if (it == nfull) {
-      absorb_tail<RL>(a, p, rem, head, aligned8);
-    }
+  for (;;) {
+    const uint32_t n = left < R ? static_cast<uint32_t>(left) : R;
+    emit_block<RL>(a, o, n);
+    left -= n;
+    if (left == 0) break;
+    o += n;
     keccak_f1600<UNROLL, FMA_MASK>(a);
-    if (it >= nfull) {
-      const uint32_t n = left < R ? static_cast<uint32_t>(left) : R;
-      emit_block<RL>(a, o, n);
-      o += n;
-      left -= n;
-    }
   }
   if (last_mask != 0xffu) {
     out[out_len - 1u] &= static_cast<uint8_t>(last_mask);
