@@ -70,7 +70,6 @@ __device__ __forceinline__ void absorb_tail(State& a, const uint8_t* p, uint32_t
                                             uint32_t head, bool aligned8) {
   if (aligned8) {
     const uint32_t fl = rem >> 3, rb = rem & 7u;
-    absorb_lanes_aligned<RL>(a, p, fl);
     const uint8_t* tp = p + 8u * fl;
     uint32_t tlo = 0u, thi = 0u;
     if (rb != 0u) {  // whole-lane messages (the common case) skip the byte loads
@@ -88,12 +87,30 @@ __device__ __forceinline__ void absorb_tail(State& a, const uint8_t* p, uint32_t
     } else {
       thi |= head << (8u * (rb - 4u));
     }
-#pragma unroll
-    for (int i = 0; i < RL; ++i) {
-      if (static_cast<uint32_t>(i) == fl) {
-        a.lo[i] ^= tlo;
-        a.hi[i] ^= thi;
-      }
+    // One statically indexed code path per number of whole lanes (jump table) instead of
+    // 2*RL predicated instructions: equal-length batches take the same case in every thread.
+    const uint2* q = reinterpret_cast<const uint2*>(p);
+    switch (fl) {
+#define B200SHA3_TAIL_CASE(K)                         \
+  case K:                                             \
+    if constexpr (K < RL) {                           \
+      _Pragma("unroll") for (int i = 0; i < K; ++i) { \
+        const uint2 v = ld_u2(q + i);                 \
+        a.lo[i] ^= v.x;                               \
+        a.hi[i] ^= v.y;                               \
+      }                                               \
+      a.lo[K < RL ? K : 0] ^= tlo;                    \
+      a.hi[K < RL ? K : 0] ^= thi;                    \
+    }                                                 \
+    break;
+      B200SHA3_TAIL_CASE(0) B200SHA3_TAIL_CASE(1) B200SHA3_TAIL_CASE(2) B200SHA3_TAIL_CASE(3)
+      B200SHA3_TAIL_CASE(4) B200SHA3_TAIL_CASE(5) B200SHA3_TAIL_CASE(6) B200SHA3_TAIL_CASE(7)
+      B200SHA3_TAIL_CASE(8) B200SHA3_TAIL_CASE(9) B200SHA3_TAIL_CASE(10) B200SHA3_TAIL_CASE(11)
+      B200SHA3_TAIL_CASE(12) B200SHA3_TAIL_CASE(13) B200SHA3_TAIL_CASE(14) B200SHA3_TAIL_CASE(15)
+      B200SHA3_TAIL_CASE(16) B200SHA3_TAIL_CASE(17) B200SHA3_TAIL_CASE(18) B200SHA3_TAIL_CASE(19)
+      B200SHA3_TAIL_CASE(20)
+#undef B200SHA3_TAIL_CASE
+      default: break;
     }
   } else {
     const uint32_t fw = rem >> 2, rb = rem & 3u;
@@ -129,17 +146,24 @@ template <int RL>
 __device__ __forceinline__ void emit_block(const State& a, uint8_t* o, uint32_t n) {
   const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(o));
   if (((mis | n) & 15u) == 0u) {
-#pragma unroll
-    for (int k = 0; k < (2 * RL + 3) / 4; ++k) {
-      if (16u * k + 16u <= n) {
-        // k indexes whole uint4 groups; lanes 2k, 2k+1 always exist for 16k+16 <= 8*RL
-        uint4 v;
-        v.x = state_word(a, (4 * k + 0 < 2 * RL) ? 4 * k + 0 : 0);
-        v.y = state_word(a, (4 * k + 1 < 2 * RL) ? 4 * k + 1 : 0);
-        v.z = state_word(a, (4 * k + 2 < 2 * RL) ? 4 * k + 2 : 0);
-        v.w = state_word(a, (4 * k + 3 < 2 * RL) ? 4 * k + 3 : 0);
-        *reinterpret_cast<uint4*>(o + 16 * k) = v;
-      }
+    // n/16 whole 16-byte stores, statically indexed per count (jump table; digests of one
+    // batch all have the same length, so every thread takes the same case).
+    uint4* dst = reinterpret_cast<uint4*>(o);
+    switch (n >> 4) {
+#define B200SHA3_EMIT_CASE(K)                                                                  \
+  case K:                                                                                      \
+    if constexpr (4 * K <= 2 * RL) {                                                           \
+      _Pragma("unroll") for (int k = 0; k < K; ++k) {                                          \
+        dst[k] = make_uint4(state_word(a, 4 * k), state_word(a, 4 * k + 1),                    \
+                            state_word(a, 4 * k + 2), state_word(a, 4 * k + 3));               \
+      }                                                                                        \
+    }                                                                                          \
+    break;
+      B200SHA3_EMIT_CASE(1) B200SHA3_EMIT_CASE(2) B200SHA3_EMIT_CASE(3) B200SHA3_EMIT_CASE(4)
+      B200SHA3_EMIT_CASE(5) B200SHA3_EMIT_CASE(6) B200SHA3_EMIT_CASE(7) B200SHA3_EMIT_CASE(8)
+      B200SHA3_EMIT_CASE(9) B200SHA3_EMIT_CASE(10)
+#undef B200SHA3_EMIT_CASE
+      default: break;
     }
   } else if ((mis & 3u) == 0u) {
 #pragma unroll
