@@ -139,44 +139,60 @@ __device__ __forceinline__ uint32_t state_word(const State& a, int j) {
   return (j & 1) ? a.hi[j >> 1] : a.lo[j >> 1];
 }
 
-// Writes the first n (<= 8*RL) bytes of the rate part, little-endian, to o.
-// 16-byte stores when o and n allow, else 4-byte stores plus a byte tail, else
-// byte stores.
+// Stores the first W whole 32-bit words of the rate part to the 4-byte aligned o, W a
+// compile-time constant: 16-byte stores while o is 16-byte aligned (VEC), else 4-byte.
+template <int RL, int W, bool VEC>
+__device__ __forceinline__ void emit_words_static(const State& a, uint8_t* o) {
+  if constexpr (W <= 2 * RL) {
+    constexpr int kVec = VEC ? W / 4 : 0;
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) {
+      reinterpret_cast<uint4*>(o)[k] = make_uint4(state_word(a, 4 * k), state_word(a, 4 * k + 1),
+                                                  state_word(a, 4 * k + 2), state_word(a, 4 * k + 3));
+    }
+#pragma unroll
+    for (int j = 4 * kVec; j < W; ++j) reinterpret_cast<uint32_t*>(o)[j] = state_word(a, j);
+  }
+}
+
+// Jump table over the number of whole words: digests of one batch all have the same
+// length, so every thread of a warp takes the same case and no predicates are needed.
+template <int RL, bool VEC>
+__device__ __forceinline__ void emit_words(const State& a, uint8_t* o, uint32_t words) {
+  switch (words) {
+#define B200SHA3_EMIT_CASE(W) \
+  case W: emit_words_static<RL, W, VEC>(a, o); break;
+#define B200SHA3_EMIT_CASES4(W) \
+  B200SHA3_EMIT_CASE(W) B200SHA3_EMIT_CASE(W + 1) B200SHA3_EMIT_CASE(W + 2) B200SHA3_EMIT_CASE(W + 3)
+    B200SHA3_EMIT_CASES4(1) B200SHA3_EMIT_CASES4(5) B200SHA3_EMIT_CASES4(9) B200SHA3_EMIT_CASES4(13)
+    B200SHA3_EMIT_CASES4(17) B200SHA3_EMIT_CASES4(21) B200SHA3_EMIT_CASES4(25) B200SHA3_EMIT_CASES4(29)
+    B200SHA3_EMIT_CASES4(33) B200SHA3_EMIT_CASES4(37) B200SHA3_EMIT_CASE(41) B200SHA3_EMIT_CASE(42)
+#undef B200SHA3_EMIT_CASES4
+#undef B200SHA3_EMIT_CASE
+    default: break;
+  }
+}
+
+// Writes the first n (<= 8*RL) bytes of the rate part, little-endian, to o: whole words
+// through the jump table above when o is 4-byte aligned (16-byte stores when it is
+// 16-byte aligned), then the 1-3 byte tail; byte stores for any other alignment.
 template <int RL>
 __device__ __forceinline__ void emit_block(const State& a, uint8_t* o, uint32_t n) {
   const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(o));
-  if (((mis | n) & 15u) == 0u) {
-    // n/16 whole 16-byte stores, statically indexed per count (jump table; digests of one
-    // batch all have the same length, so every thread takes the same case).
-    uint4* dst = reinterpret_cast<uint4*>(o);
-    switch (n >> 4) {
-#define B200SHA3_EMIT_CASE(K)                                                                  \
-  case K:                                                                                      \
-    if constexpr (4 * K <= 2 * RL) {                                                           \
-      _Pragma("unroll") for (int k = 0; k < K; ++k) {                                          \
-        dst[k] = make_uint4(state_word(a, 4 * k), state_word(a, 4 * k + 1),                    \
-                            state_word(a, 4 * k + 2), state_word(a, 4 * k + 3));               \
-      }                                                                                        \
-    }                                                                                          \
-    break;
-      B200SHA3_EMIT_CASE(1) B200SHA3_EMIT_CASE(2) B200SHA3_EMIT_CASE(3) B200SHA3_EMIT_CASE(4)
-      B200SHA3_EMIT_CASE(5) B200SHA3_EMIT_CASE(6) B200SHA3_EMIT_CASE(7) B200SHA3_EMIT_CASE(8)
-      B200SHA3_EMIT_CASE(9) B200SHA3_EMIT_CASE(10)
-#undef B200SHA3_EMIT_CASE
-      default: break;
+  if ((mis & 3u) == 0u) {
+    const uint32_t words = n >> 2, tail = n & 3u;
+    if ((mis & 15u) == 0u) {
+      emit_words<RL, true>(a, o, words);
+    } else {
+      emit_words<RL, false>(a, o, words);
     }
-  } else if ((mis & 3u) == 0u) {
+    if (tail != 0u) {  // XOF lengths that are not a multiple of 4 bytes
+      uint32_t w = 0u;
 #pragma unroll
-    for (int j = 0; j < 2 * RL; ++j) {
-      const uint32_t w = state_word(a, j);
-      if (4u * j + 4u <= n) {
-        *reinterpret_cast<uint32_t*>(o + 4 * j) = w;
-      } else if (4u * j < n) {
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          if (4u * j + b < n) o[4 * j + b] = static_cast<uint8_t>(w >> (8 * b));
-        }
+      for (int j = 0; j < 2 * RL; ++j) {
+        if (static_cast<uint32_t>(j) == words) w = state_word(a, j);
       }
+      for (uint32_t b = 0; b < tail; ++b) o[4u * words + b] = static_cast<uint8_t>(w >> (8u * b));
     }
   } else {
 #pragma unroll
