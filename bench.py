@@ -115,14 +115,24 @@ class ClockSampler:
 
 
 def host_memory_available():
-    """MemAvailable in bytes (0 if unknown)."""
+    """Bytes of host memory this process can still take: MemAvailable, capped by the cgroup
+    limit when there is one (0 if unknown)."""
+    avail = 0
     try:
         for line in open("/proc/meminfo"):
             if line.startswith("MemAvailable:"):
-                return int(line.split()[1]) * 1024
+                avail = int(line.split()[1]) * 1024
     except OSError:
         pass
-    return 0
+    try:
+        limit = open("/sys/fs/cgroup/memory.max").read().strip()
+        used = int(open("/sys/fs/cgroup/memory.current").read().strip())
+        if limit != "max":
+            room = max(int(limit) - used, 0)
+            avail = min(avail, room) if avail else room
+    except (OSError, ValueError):
+        pass
+    return avail
 
 
 def measured_peaks():
