@@ -107,3 +107,23 @@ def test_product_never_touches_the_oracle():
                 if re.search(r"oracle|keccak_oracle|libsha3kit_ref|/root/reference", text):
                     offenders.append(str(path.relative_to(ROOT)))
     assert offenders == []
+
+
+def test_misc_queries_without_a_device():
+    import ctypes as C
+    from paper_1902_05320_b200 import library_path
+    lib = C.CDLL(str(library_path()))
+    lib.b200sha3_version.restype = C.c_char_p
+    lib.b200sha3_strerror.restype = C.c_char_p
+    lib.b200sha3_strerror.argtypes = [C.c_int]
+    assert b"sm_100a" in lib.b200sha3_version()
+    assert lib.b200sha3_device_count() >= 0
+    texts = {lib.b200sha3_strerror(i) for i in range(5)}
+    assert len(texts) == 5 and b"unknown status" not in texts
+    assert lib.b200sha3_strerror(99) == b"unknown status"
+    # handles: bad algorithm is rejected before CUDA is touched; NULL handle calls are safe
+    handle = C.c_void_p()
+    lib.b200sha3_states_create.argtypes = [C.c_int, C.c_uint64, C.c_void_p, C.POINTER(C.c_void_p)]
+    assert lib.b200sha3_states_create(7, 4, None, C.byref(handle)) == 1 and not handle.value
+    lib.b200sha3_states_destroy.argtypes = [C.c_void_p]
+    assert lib.b200sha3_states_destroy(None) == 0
