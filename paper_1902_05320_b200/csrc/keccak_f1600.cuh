@@ -215,6 +215,7 @@ __device__ __forceinline__ void keccak_round(State& a, uint32_t rc_lo, uint32_t 
 //   UNROLL = 22  "peeled": rounds 0 and 23 straight-line (so the same dead-work removal
 //                applies to them), rounds 1..22 in a loop of two rounds per body that
 //                stays I-cache resident (the 67 KB fully unrolled body does not).
+//   UNROLL = 21  round 0 and rounds 22-23 straight-line, rounds 1..21 as 3 x 7.
 //   UNROLL = 1, 2, 4  plain loop, constants from the constant bank.
 template <int UNROLL, uint32_t FMA_MASK>
 __device__ __forceinline__ void keccak_f1600(State& a) {
@@ -232,6 +233,23 @@ __device__ __forceinline__ void keccak_f1600(State& a) {
       keccak_round<FMA_MASK>(a, kRoundConst32[2 * r], kRoundConst32[2 * r + 1]);
       keccak_round<FMA_MASK>(a, kRoundConst32[2 * r + 2], kRoundConst32[2 * r + 3]);
     }
+    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(23)),
+                           static_cast<uint32_t>(round_constant(23) >> 32));
+  } else if constexpr (UNROLL == 21) {
+    // Round 0 and rounds 22, 23 straight-line, rounds 1..21 as three iterations of seven:
+    // ~29 KB of code (fits the 32 KB instruction cache level that the 67 KB fully unrolled
+    // body overflows) with the same dead-work removal on entry and exit.
+    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(0)),
+                           static_cast<uint32_t>(round_constant(0) >> 32));
+#pragma unroll 1
+    for (int r = 1; r < 22; r += 7) {
+#pragma unroll
+      for (int u = 0; u < 7; ++u) {
+        keccak_round<FMA_MASK>(a, kRoundConst32[2 * (r + u)], kRoundConst32[2 * (r + u) + 1]);
+      }
+    }
+    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(22)),
+                           static_cast<uint32_t>(round_constant(22) >> 32));
     keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(23)),
                            static_cast<uint32_t>(round_constant(23) >> 32));
   } else {

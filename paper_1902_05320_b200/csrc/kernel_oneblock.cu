@@ -53,6 +53,7 @@ cudaError_t launch_hash_oneblock(const HashArgs& args, const LaunchPlan& plan,
   switch (plan.unroll) {
     case 2: return launch_sha3_256_64<2>(args, plan, stream);
     case 4: return launch_sha3_256_64<4>(args, plan, stream);
+    case 21: return launch_sha3_256_64<21>(args, plan, stream);
     case 22: return launch_sha3_256_64<22>(args, plan, stream);
     case 24: return launch_sha3_256_64<24>(args, plan, stream);
     default: return cudaErrorNotSupported;
