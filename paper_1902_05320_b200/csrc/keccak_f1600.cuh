@@ -209,13 +209,41 @@ __device__ __forceinline__ void keccak_round(State& a, uint32_t rc_lo, uint32_t 
 
 #undef B200SHA3_RHOPI
 
+// HEAD straight-line rounds, ITERS iterations of BODY rounds, then the remaining rounds
+// straight-line.  The straight-line head and tail let ptxas drop the work on lanes that are
+// known zero on entry and on lanes nobody reads on exit, exactly as in the fully unrolled
+// form, while the loop keeps the code inside the instruction cache.
+template <int HEAD, int BODY, int ITERS, uint32_t FMA_MASK>
+__device__ __forceinline__ void keccak_f1600_peeled(State& a) {
+  constexpr int kTailStart = HEAD + BODY * ITERS;
+  static_assert(kTailStart <= 24, "too many rounds");
+#pragma unroll
+  for (int r = 0; r < HEAD; ++r) {
+    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(r)),
+                           static_cast<uint32_t>(round_constant(r) >> 32));
+  }
+#pragma unroll 1
+  for (int r = HEAD; r < kTailStart; r += BODY) {
+#pragma unroll
+    for (int u = 0; u < BODY; ++u) {
+      keccak_round<FMA_MASK>(a, kRoundConst32[2 * (r + u)], kRoundConst32[2 * (r + u) + 1]);
+    }
+  }
+#pragma unroll
+  for (int r = kTailStart; r < 24; ++r) {
+    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(r)),
+                           static_cast<uint32_t>(round_constant(r) >> 32));
+  }
+}
+
 // 24 rounds.
 //   UNROLL = 24  straight-line code with immediates; ptxas also drops the work on lanes
 //                that are known zero on entry and on lanes nobody reads on exit.
 //   UNROLL = 22  "peeled": rounds 0 and 23 straight-line (so the same dead-work removal
 //                applies to them), rounds 1..22 in a loop of two rounds per body that
 //                stays I-cache resident (the 67 KB fully unrolled body does not).
-//   UNROLL = 21  round 0 and rounds 22-23 straight-line, rounds 1..21 as 3 x 7.
+//   UNROLL = 21, 20, 23, 11  peeled forms (see keccak_f1600_peeled): head + iterations x
+//                body + tail = 1 + 3x7 + 2, 1 + 4x5 + 3, 1 + 7x3 + 2, 1 + 2x11 + 1.
 //   UNROLL = 1, 2, 4  plain loop, constants from the constant bank.
 template <int UNROLL, uint32_t FMA_MASK>
 __device__ __forceinline__ void keccak_f1600(State& a) {
@@ -226,32 +254,15 @@ __device__ __forceinline__ void keccak_f1600(State& a) {
                              static_cast<uint32_t>(round_constant(r) >> 32));
     }
   } else if constexpr (UNROLL == 22) {
-    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(0)),
-                           static_cast<uint32_t>(round_constant(0) >> 32));
-#pragma unroll 1
-    for (int r = 1; r < 23; r += 2) {
-      keccak_round<FMA_MASK>(a, kRoundConst32[2 * r], kRoundConst32[2 * r + 1]);
-      keccak_round<FMA_MASK>(a, kRoundConst32[2 * r + 2], kRoundConst32[2 * r + 3]);
-    }
-    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(23)),
-                           static_cast<uint32_t>(round_constant(23) >> 32));
+    keccak_f1600_peeled<1, 2, 11, FMA_MASK>(a);  // 1 + 11 x 2 + 1, ~10 KB
   } else if constexpr (UNROLL == 21) {
-    // Round 0 and rounds 22, 23 straight-line, rounds 1..21 as three iterations of seven:
-    // ~29 KB of code (fits the 32 KB instruction cache level that the 67 KB fully unrolled
-    // body overflows) with the same dead-work removal on entry and exit.
-    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(0)),
-                           static_cast<uint32_t>(round_constant(0) >> 32));
-#pragma unroll 1
-    for (int r = 1; r < 22; r += 7) {
-#pragma unroll
-      for (int u = 0; u < 7; ++u) {
-        keccak_round<FMA_MASK>(a, kRoundConst32[2 * (r + u)], kRoundConst32[2 * (r + u) + 1]);
-      }
-    }
-    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(22)),
-                           static_cast<uint32_t>(round_constant(22) >> 32));
-    keccak_round<FMA_MASK>(a, static_cast<uint32_t>(round_constant(23)),
-                           static_cast<uint32_t>(round_constant(23) >> 32));
+    keccak_f1600_peeled<1, 7, 3, FMA_MASK>(a);   // 1 + 3 x 7 + 2, ~29 KB of code
+  } else if constexpr (UNROLL == 20) {
+    keccak_f1600_peeled<1, 5, 4, FMA_MASK>(a);   // 1 + 4 x 5 + 3, ~26 KB
+  } else if constexpr (UNROLL == 23) {
+    keccak_f1600_peeled<1, 3, 7, FMA_MASK>(a);   // 1 + 7 x 3 + 2, ~17 KB
+  } else if constexpr (UNROLL == 11) {
+    keccak_f1600_peeled<1, 11, 2, FMA_MASK>(a);  // 1 + 2 x 11 + 1, ~37 KB
   } else {
     static_assert(24 % UNROLL == 0, "UNROLL must divide 24");
 #pragma unroll 1

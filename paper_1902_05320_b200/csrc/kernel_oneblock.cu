@@ -47,13 +47,16 @@ cudaError_t launch_hash_oneblock(const HashArgs& args, const LaunchPlan& plan,
   }
   const int ml = static_cast<int>(args.fixed_len / 8), ow = static_cast<int>(args.digest_bytes / 4);
   if (!(plan.rate_lanes == 17 && ml == 8 && ow == 8)) {
-    // every other shape exists only as UNROLL 24 / ALU-only
+    // every other shape exists only as UNROLL 21 / ALU-only
     return launch_oneblock_shape(plan.rate_lanes, ml, ow, args, plan, stream);
   }
   switch (plan.unroll) {
     case 2: return launch_sha3_256_64<2>(args, plan, stream);
     case 4: return launch_sha3_256_64<4>(args, plan, stream);
+    case 11: return launch_sha3_256_64<11>(args, plan, stream);
+    case 20: return launch_sha3_256_64<20>(args, plan, stream);
     case 21: return launch_sha3_256_64<21>(args, plan, stream);
+    case 23: return launch_sha3_256_64<23>(args, plan, stream);
     case 22: return launch_sha3_256_64<22>(args, plan, stream);
     case 24: return launch_sha3_256_64<24>(args, plan, stream);
     default: return cudaErrorNotSupported;

@@ -57,7 +57,7 @@ hash_oneblock_kernel(const uint8_t* __restrict__ data, uint8_t* __restrict__ dig
 template <int RL, int ML, int OW, int UNROLL, int PRESET>
 cudaError_t launch_oneblock_instance(const HashArgs& args, const LaunchPlan& plan,
                                      cudaStream_t stream) {
-  const int threads = plan.block_threads > 0 ? plan.block_threads : 256;
+  const int threads = plan.block_threads > 0 ? plan.block_threads : 128;
   const uint64_t blocks = (args.count + threads - 1) / threads;
   if (blocks == 0) return cudaSuccess;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
@@ -67,8 +67,8 @@ cudaError_t launch_oneblock_instance(const HashArgs& args, const LaunchPlan& pla
   return cudaGetLastError();
 }
 
-// Shapes other than the tuning-matrix one (kernel_oneblock_shapes.cu): UNROLL 24,
-// ALU only.  Returns cudaErrorNotSupported when (rl, ml, ow) is not instantiated.
+// Shapes other than the tuning-matrix one (kernel_oneblock_shapes.cu): UNROLL 21 (the
+// measured best), ALU only.  Returns cudaErrorNotSupported when (rl, ml, ow) is not instantiated.
 cudaError_t launch_oneblock_shape(int rl, int ml, int ow, const HashArgs& args,
                                   const LaunchPlan& plan, cudaStream_t stream);
 bool oneblock_shape_exists(int rl, int ml, int ow);

@@ -45,9 +45,9 @@ def main():
     count = 1 << (int(sys.argv[1]) if len(sys.argv) > 1 else 24)
     dev = e.generate_workload(count * 64, 64, seed=1)
     ref = Engine(kernel=KERNEL_GENERIC).hash_fixed("sha3_256", dev, 64, count)
-    for kernel, kname, unrolls in ((KERNEL_ONEBLOCK, "oneblock", (2, 21, 22, 24)), (KERNEL_GENERIC, "generic", (2,))):
+    for kernel, kname, unrolls in ((KERNEL_ONEBLOCK, "oneblock", (2, 11, 20, 21, 22, 23, 24)), (KERNEL_GENERIC, "generic", (2,))):
         for unroll in unrolls:
-            for preset in ((0, 8) if kernel == KERNEL_ONEBLOCK else (0,)):
+            for preset in (0,):
                 for threads in ((64, 128, 256) if preset == 0 else (128,)):
                     eng = Engine(kernel=kernel, unroll=unroll, fma_preset=preset, block_threads=threads)
                     ms = time_hash(eng, dev, count)
