@@ -370,7 +370,7 @@ def main():
                                    f"over {world} GPU(s) by contiguous ranges (BASELINE.json configs[4])",
                        "messages_total": total, "messages_per_gpu": count, "message_bytes": MSG_LEN,
                        "l2_policy": "inputs larger than L2 (%.1f GiB per GPU per step)" % (count * MSG_LEN / 2**30),
-                       "kernel": "hash_oneblock_kernel<17,8,8,UNROLL=21 (peeled 1+3x7+2),ALU-only>"},
+                       "kernel": "hash_oneblock_kernel<17,8,8,UNROLL=23 (peeled 1+7x3+2),ALU-only>"},
             "gb_per_s_hashed": value * MSG_LEN / 1e9,
             "gpu_launches": launches,
             "digest_checksum": f"{checksum:016x}",

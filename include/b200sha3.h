@@ -105,7 +105,7 @@ typedef struct b200sha3_config {
   void* stream;            /* cudaStream_t to enqueue on; NULL = the default stream */
   uint32_t flags;          /* B200SHA3_FLAG_*                                        */
   int32_t kernel;          /* B200SHA3_KERNEL_*                                      */
-  int32_t unroll;          /* one-block kernel: 0 = default, else 2, 4, 21/22 (peeled), 24 */
+  int32_t unroll;          /* one-block kernel: 0 = default; 2, 4 rolled; 11, 20..23 peeled; 24 full */
   int32_t fma_preset;      /* -1 = default; 0..8 = FMA-pipe rotation offload preset  */
   int32_t block_threads;   /* 0 = default                                            */
   /* If non-NULL receives the device time of the hashing phase in milliseconds

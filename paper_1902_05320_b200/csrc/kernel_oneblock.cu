@@ -47,7 +47,7 @@ cudaError_t launch_hash_oneblock(const HashArgs& args, const LaunchPlan& plan,
   }
   const int ml = static_cast<int>(args.fixed_len / 8), ow = static_cast<int>(args.digest_bytes / 4);
   if (!(plan.rate_lanes == 17 && ml == 8 && ow == 8)) {
-    // every other shape exists only as UNROLL 21 / ALU-only
+    // every other shape exists only as UNROLL 23 / ALU-only
     return launch_oneblock_shape(plan.rate_lanes, ml, ow, args, plan, stream);
   }
   switch (plan.unroll) {

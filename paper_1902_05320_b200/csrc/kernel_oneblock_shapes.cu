@@ -1,7 +1,7 @@
 // kernel_oneblock_shapes.cu -- single-block kernel instantiations for the other
 // fixed-length shapes of BASELINE.json cfg2 / cfg3: 32-, 64- and 128-byte
 // messages for every variant whose rate leaves room for the pad byte, with the
-// variant's digest (or 32 / 64 / 128 bytes of SHAKE output).  UNROLL 21, ALU only.
+// variant's digest (or 32 / 64 / 128 bytes of SHAKE output).  UNROLL 23 (peeled 1 + 7x3 + 2), ALU only.
 #include "oneblock.cuh"
 
 namespace b200sha3 {
@@ -29,7 +29,7 @@ cudaError_t launch_oneblock_shape(int rl, int ml, int ow, const HashArgs& args,
                                   const LaunchPlan& plan, cudaStream_t stream) {
 #define X(RL, ML, OW)                      \
   if (rl == RL && ml == ML && ow == OW)    \
-    return launch_oneblock_instance<RL, ML, OW, 21, 0>(args, plan, stream);
+    return launch_oneblock_instance<RL, ML, OW, 23, 0>(args, plan, stream);
   B200SHA3_SHAPES(X)
 #undef X
   return cudaErrorNotSupported;

@@ -67,8 +67,8 @@ cudaError_t launch_oneblock_instance(const HashArgs& args, const LaunchPlan& pla
   return cudaGetLastError();
 }
 
-// Shapes other than the tuning-matrix one (kernel_oneblock_shapes.cu): UNROLL 21 (the
-// measured best), ALU only.  Returns cudaErrorNotSupported when (rl, ml, ow) is not instantiated.
+// Shapes other than the tuning-matrix one (kernel_oneblock_shapes.cu): UNROLL 23 (peeled
+// 1 + 7x3 + 2, the measured best), ALU only.  Returns cudaErrorNotSupported when (rl, ml, ow) is not instantiated.
 cudaError_t launch_oneblock_shape(int rl, int ml, int ow, const HashArgs& args,
                                   const LaunchPlan& plan, cudaStream_t stream);
 bool oneblock_shape_exists(int rl, int ml, int ow);
