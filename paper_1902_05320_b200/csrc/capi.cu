@@ -98,7 +98,7 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
   } else if (kernel == B200SHA3_KERNEL_STAGED) {
     err = launch_hash_staged(args, plan, stream);
   } else {
-    plan.unroll = 2;
+    plan.unroll = c.unroll;  // 0 = the kernel's default loop shape
     plan.fma_preset = c.fma_preset >= 0 ? c.fma_preset : kDefaultFmaGeneric;
     err = launch_hash_generic(args, plan, stream);
   }
@@ -171,7 +171,7 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     args.last_mask = last_byte_mask(algorithm, xof_bits);
     LaunchPlan plan{};
     plan.rate_lanes = v.rate_lanes;
-    plan.unroll = 2;
+    plan.unroll = c.unroll;  // 0 = the kernel's default loop shape
     plan.fma_preset = c.fma_preset >= 0 ? c.fma_preset : kDefaultFmaGeneric;
     plan.block_threads = c.block_threads;
     cudaError_t err = c.kernel == B200SHA3_KERNEL_STAGED ? launch_hash_staged(args, plan, stream)

@@ -12,6 +12,8 @@ namespace b200sha3 {
 
 namespace {
 
+constexpr int kGenericUnroll = 3;  // rounds per loop body (8 iterations)
+
 template <int RL, int UNROLL, uint32_t FMA_MASK>
 __global__ void __launch_bounds__(256, 2)
 hash_generic_kernel(const HashArgs args) {
@@ -40,12 +42,20 @@ cudaError_t launch_one(const HashArgs& args, const LaunchPlan& plan, cudaStream_
 
 template <int RL>
 cudaError_t launch_rl(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {
-  // Generic kernel instantiations: rolled loop (2 rounds per body); ALU only (the
+  // Generic kernel instantiations: plain loop, kGenericUnroll rounds per body; ALU only (the
   // default) or FMA preset 5 (every rho rotation on the FMA pipe), kept for the measured
-  // comparison of DESIGN.md section 4.
+  // comparison of DESIGN.md section 4.  SHA3-256's rate also carries the loop-shape sweep.
+  if constexpr (RL == 17) {
+    switch (plan.unroll) {
+      case 2: return launch_one<RL, 2, 0>(args, plan, stream);
+      case 4: return launch_one<RL, 4, 0>(args, plan, stream);
+      case 6: return launch_one<RL, 6, 0>(args, plan, stream);
+      default: break;
+    }
+  }
   switch (plan.fma_preset) {
-    case 0: return launch_one<RL, 2, 0>(args, plan, stream);
-    default: return launch_one<RL, 2, 5>(args, plan, stream);
+    case 0: return launch_one<RL, kGenericUnroll, 0>(args, plan, stream);
+    default: return launch_one<RL, kGenericUnroll, 5>(args, plan, stream);
   }
 }
 
