@@ -75,6 +75,17 @@ class DeviceError : public std::runtime_error {
   int status_;
 };
 
+// Where the wall clock of one hash_batch call went (optional, see DeviceConfig::stages).
+// The call is a software pipeline (host/batch_adapter.cpp): `scan` (message sizes, plan,
+// staging) runs first, then pack tasks, C-ABI calls (H2D + kernels + D2H, one per ~32 MiB
+// chunk) and unpack tasks overlap for `pipeline` seconds; `resize` is the value-initialisation
+// of the outer digest vector (one thread, overlapped with packing).  `*_cpu` are summed over
+// the threads that ran the tasks, `device_calls` over the chunks.
+struct StageTimes {
+  double scan = 0, pipeline = 0, resize = 0, device_calls = 0, pack_cpu = 0, unpack_cpu = 0;
+  unsigned threads = 0, chunks = 0, tasks = 0;
+};
+
 // Device-side knobs that EngineConfig has no field for.
 struct DeviceConfig {
   int device = -1;           // CUDA ordinal, -1 = current
@@ -86,6 +97,7 @@ struct DeviceConfig {
   // plan_partition (batch.cpp:46-62) one level up; no inter-device traffic, digests land
   // in message order.  `device` and `stream` are then ignored.
   std::vector<int> devices;
+  StageTimes* stages = nullptr;  // filled when non-null (profiling aid)
 
   // Every CUDA device visible to the process.
   static DeviceConfig all_devices();

@@ -5,6 +5,7 @@
 // reference's own translation units, compiled from /root/reference where they
 // lie.  Used (a) to validate the C restatement in keccak_oracle.c, and (b) as
 // the CPU baseline (`cpu_baseline.kind = "reference"`) in bench.py.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <new>
@@ -94,6 +95,28 @@ __attribute__((visibility("default"))) int ref_batch_run(void* handle, int backe
   if (!handle) return 2;
   return run_batch(*static_cast<sha3::HashBatch*>(handle), backend, workers, chunk, out,
                    elapsed);
+}
+
+// Wall clock of the reference's hash_batch call alone (slot allocation, batch.cpp:77-81,
+// included; the result's destruction excluded) next to BatchResult::elapsed.
+__attribute__((visibility("default"))) int ref_batch_run_wall(void* handle, unsigned workers,
+                                                              double* call_wall,
+                                                              double* elapsed) {
+  if (!handle) return 2;
+  try {
+    sha3::EngineConfig cfg;
+    cfg.backend = sha3::Backend::parallel;
+    cfg.workers = workers;
+    const auto t0 = std::chrono::steady_clock::now();
+    const sha3::BatchResult res = sha3::hash_batch(*static_cast<sha3::HashBatch*>(handle), cfg);
+    if (call_wall) {
+      *call_wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    if (elapsed) *elapsed = res.elapsed.count();
+    return 0;
+  } catch (...) {
+    return 2;
+  }
 }
 
 __attribute__((visibility("default"))) void ref_batch_destroy(void* handle) {

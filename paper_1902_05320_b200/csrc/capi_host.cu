@@ -52,13 +52,18 @@ class StreamCache {
 
 thread_local StreamCache t_streams;
 
-uint64_t chunk_target_bytes() {
-  static const uint64_t value = [] {
+// One message is one thread, so a chunk must also carry enough MESSAGES to fill the GPU: for
+// long messages the byte target grows until a chunk holds ~2^16 of them (2048 warps), up to
+// 1 GiB (three slots of that are still < 2 % of the HBM).
+uint64_t chunk_target_bytes(uint64_t avg_message_bytes) {
+  static const long env_mib = [] {
     const char* env = std::getenv("B200SHA3_CHUNK_MIB");
-    const long mib = env ? std::atol(env) : 0;
-    return static_cast<uint64_t>(mib > 0 ? mib : 64) << 20;
+    return env ? std::atol(env) : 0L;
   }();
-  return value;
+  if (env_mib > 0) return static_cast<uint64_t>(env_mib) << 20;
+  const uint64_t base = 64ull << 20, cap = 1ull << 30;
+  const uint64_t want = avg_message_bytes > (cap >> 16) ? cap : avg_message_bytes << 16;
+  return std::min(std::max(want, base), cap);
 }
 
 // Three pipeline slots, each a stream plus the device buffers of the chunk it currently
@@ -231,7 +236,8 @@ int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_t msg_len, ui
   if (c.stream) CU(cudaStreamSynchronize(c.stream));
 
   const bool pipelined = (c.flags & B200SHA3_FLAG_NO_PIPELINE) == 0;
-  uint64_t chunk = pipelined ? chunk_target_bytes() / std::max<uint64_t>(1, msg_len + digest_bytes) : count;
+  const uint64_t unit = std::max<uint64_t>(1, msg_len + digest_bytes);
+  uint64_t chunk = pipelined ? chunk_target_bytes(unit) / unit : count;
   chunk = std::min(std::max<uint64_t>(chunk, 16), count);
   SlotPipeline pipe(chunk < count ? kPipelineSlots : 1, c.device_ms != nullptr);
   CU(pipe.init());
@@ -283,8 +289,11 @@ int b200sha3_hash_batch(int algorithm, const uint8_t* data, const uint64_t* offs
   if (!digests || !offsets || !lengths) return B200SHA3_ERR_INVALID_ARGUMENT;
 
   std::vector<HostChunk> chunks;
+  // average message size of a packed batch: the span from the first to the last message
+  const uint64_t span = offsets[count - 1] + lengths[count - 1] - std::min(offsets[0], offsets[count - 1]);
   const bool pipelined = (c.flags & B200SHA3_FLAG_NO_PIPELINE) == 0 &&
-                         plan_ordered_chunks(offsets, lengths, count, chunk_target_bytes(), &chunks);
+                         plan_ordered_chunks(offsets, lengths, count,
+                                             chunk_target_bytes(span / count + digest_bytes), &chunks);
   if (!pipelined) chunks.assign(1, whole_batch_chunk(offsets, lengths, count));
   uint64_t max_span = 0, max_count = 0;
   for (const HostChunk& ch : chunks) {

@@ -5,11 +5,20 @@
 #include "b200sha3/batch.hpp"
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <thread>
+
+#if defined(__linux__)
+#include <sys/mman.h>
+#endif
 
 namespace sha3::b200 {
 
@@ -94,6 +103,21 @@ class StagingBuffer {
 constexpr std::uint64_t kKeepBytes = 2ull << 30;
 thread_local StagingBuffer t_data_staging, t_digest_staging;
 
+// Asks for transparent huge pages on the whole pages inside [p, p + bytes): a hint on memory
+// the caller owns, ignored where the kernel has THP off.
+void advise_huge_pages(void* p, std::size_t bytes) {
+#if defined(__linux__) && defined(MADV_HUGEPAGE)
+  constexpr std::uintptr_t kHuge = std::uintptr_t{2} << 20;
+  if (bytes < 2 * kHuge) return;
+  const std::uintptr_t lo = (reinterpret_cast<std::uintptr_t>(p) + kHuge - 1) & ~(kHuge - 1);
+  const std::uintptr_t hi = (reinterpret_cast<std::uintptr_t>(p) + bytes) & ~(kHuge - 1);
+  if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+#else
+  (void)p;
+  (void)bytes;
+#endif
+}
+
 b200sha3_config make_config(const DeviceConfig& device, double* ms) {
   b200sha3_config cfg{};
   cfg.struct_size = sizeof cfg;
@@ -131,6 +155,398 @@ std::vector<std::uint8_t> hash_packed(Algorithm algorithm, const std::uint8_t* d
   return out;
 }
 
+// ---------------------------------------------------------------------------------------
+// hash_batch as a software pipeline.
+//
+// The reference's call is "allocate the digest slots, then hash" (batch.cpp:77-133).  On the
+// GPU the hashing itself is a few percent of the call; the rest is moving bytes between
+// vector<vector<uint8_t>> and the packed buffers of the C ABI.  So the call is cut into
+//   scan    sizes of all messages -> equal-length or ragged, byte totals per block of messages
+//   tasks   ~1 MiB each: pack (messages -> pinned staging) and unpack (pinned digests -> slots)
+//   chunks  ~32 MiB each: one C-ABI call (H2D, kernels, D2H) per chunk, as soon as it is packed
+// and run by `workers` threads (batch.hpp:15-19; the caller takes part, batch.cpp:126) that pull
+// work from one scheduler: device calls first, then packing, then unpacking, so copies and
+// kernels of chunk k overlap the packing of chunk k+1 and the unpacking of chunk k-1.  The
+// value-initialisation of the outer digest vector -- inherently one thread -- is one more task
+// that overlaps the packing.  With several devices, chunk k goes to device k mod n, each device
+// driven by its own host thread; digests land in message order whatever the schedule.
+class BatchPipeline {
+ public:
+  BatchPipeline(const HashBatch& batch, const EngineConfig& config, const DeviceConfig& device,
+                std::uint64_t digest_bytes, BatchResult& result)
+      : batch_(batch), device_(device), alg_(static_cast<int>(batch.algorithm)),
+        digest_bytes_(digest_bytes), workers_(pack_workers(config)), result_(result),
+        count_(batch.messages.size()) {}
+
+  void run() {
+    const auto t0 = clock::now();
+    block_msgs_ = std::max<std::size_t>(1, std::min<std::size_t>(256, count_ / 1024));
+    nblocks_ = (count_ + block_msgs_ - 1) / block_msgs_;
+    first_len_ = batch_.messages[0].size();
+    nsteps_ = (count_ + kResizeStep - 1) / kResizeStep;
+    step_state_.reset(new std::atomic<std::uint8_t>[nsteps_]);
+    for (std::size_t i = 0; i < nsteps_; ++i) step_state_[i].store(kStepUntouched);
+    // Large batches whose sampled sizes all agree are taken as equal-length without reading
+    // every size first: the pack tasks check as they copy, and a mismatch restarts the call on
+    // the ragged layout.  (generate_workload batches, workload.cpp:34-45, never restart.)
+    speculative_ = count_ >= kParallelScanMin && sample_is_fixed();
+    if (!speculative_) scan();
+    plan();
+    double scan_s = since(t0);
+    run_threads();
+    if (mismatch_.load() && !failed_) {
+      const auto t2 = clock::now();
+      speculative_ = false;
+      mismatch_.store(false);
+      scan();
+      plan();
+      scan_s += since(t2);
+      run_threads();
+    }
+    t_data_staging.trim(failed_ ? 0 : kKeepBytes);
+    t_digest_staging.trim(failed_ ? 0 : kKeepBytes);
+    if (error_) std::rethrow_exception(error_);  // first failure wins (batch.cpp:111-130)
+    double ms = 0.0;
+    for (double d : device_ms_) ms = std::max(ms, d);
+    result_.elapsed = std::chrono::duration<double>(ms * 1e-3);
+    if (StageTimes* st = device_.stages) {
+      st->scan = scan_s;
+      st->pipeline = since(t0) - scan_s;
+      st->resize = resize_s_;
+      st->device_calls = device_calls_s_;
+      st->pack_cpu = pack_cpu_s_;
+      st->unpack_cpu = unpack_cpu_s_;
+      st->threads = threads_;
+      st->chunks = static_cast<unsigned>(nchunks_);
+      st->tasks = static_cast<unsigned>(ntasks_);
+    }
+  }
+
+ private:
+  using clock = std::chrono::steady_clock;
+  static double since(clock::time_point t) {
+    return std::chrono::duration<double>(clock::now() - t).count();
+  }
+  static std::uint64_t pad8(std::uint64_t n) { return (n + 7) & ~std::uint64_t{7}; }
+
+  static constexpr std::uint64_t kTaskBytes = 1ull << 20;      // input + output per task
+  static constexpr std::uint64_t kChunkBytes = 32ull << 20;    // input + output per device call ...
+  static constexpr std::uint64_t kChunkMinMessages = 1u << 15; // ... grown to hold this many messages
+  static constexpr std::uint64_t kMaxChunkBytes = 1ull << 30;  // ... up to this
+  static constexpr std::uint64_t kPoolMinBytes = 4ull << 20;   // below: the caller works alone
+  static constexpr std::size_t kParallelScanMin = 1u << 18;    // messages
+  static constexpr std::size_t kRingChunks = 12;               // pinned staging: chunks in flight
+  static constexpr std::uint64_t kRingBytes = 1ull << 30;      // ... and their bytes, at most
+  static constexpr std::size_t kResizeStep = 1u << 17;         // digest slots per published step
+  static constexpr std::uint8_t kStepUntouched = 0, kStepTouching = 1, kStepBuilt = 2;
+
+  bool sample_is_fixed() const {
+    const std::size_t head = std::min<std::size_t>(count_, 256), stride = count_ / 256;
+    for (std::size_t i = 0; i < head; ++i) {
+      if (batch_.messages[i].size() != first_len_) return false;
+      if (batch_.messages[i * stride].size() != first_len_) return false;
+    }
+    return batch_.messages[count_ - 1].size() == first_len_;
+  }
+
+  // Sizes of all messages, per block of block_msgs_ messages: padded byte total and whether
+  // every length equals the first message's.
+  void scan() {
+    block_base_.reset(new std::uint64_t[nblocks_ + 1]);
+    std::unique_ptr<bool[]> block_fixed(new bool[nblocks_]);
+    const auto scan_blocks = [&](std::size_t begin, std::size_t end) {
+      for (std::size_t b = begin; b < end; ++b) {
+        const std::size_t lo = b * block_msgs_, hi = std::min(count_, lo + block_msgs_);
+        std::uint64_t bytes = 0;
+        bool same = true;
+        for (std::size_t i = lo; i < hi; ++i) {
+          const std::uint64_t len = batch_.messages[i].size();
+          same = same && len == first_len_;
+          bytes += pad8(len);
+        }
+        block_base_[b + 1] = bytes;
+        block_fixed[b] = same;
+      }
+    };
+    parallel_ranges(nblocks_, count_ >= kParallelScanMin ? workers_ : 1, ~std::uint64_t{0}, scan_blocks);
+    fixed_ = true;
+    block_base_[0] = 0;
+    for (std::size_t b = 0; b < nblocks_; ++b) {
+      fixed_ = fixed_ && block_fixed[b];
+      block_base_[b + 1] += block_base_[b];  // exclusive prefix: where block b starts (ragged layout)
+    }
+  }
+
+  // Equal-length batches (what generate_workload builds, workload.cpp:34-45) go back to back
+  // and take the fixed-length entry: no offset table, no bucketing pass.  Ragged batches get
+  // 8-byte aligned offsets so the device can use aligned 64-bit loads.
+  void plan() {
+    if (speculative_) fixed_ = true;
+    total_in_ = fixed_ ? count_ * first_len_ : block_base_[nblocks_];
+    const std::uint64_t total = total_in_ + count_ * digest_bytes_;
+    const std::uint64_t block_bytes = std::max<std::uint64_t>(1, total / nblocks_);
+    task_blocks_ = std::max<std::size_t>(1, std::min<std::uint64_t>(kTaskBytes / block_bytes, nblocks_));
+    ntasks_ = (nblocks_ + task_blocks_ - 1) / task_blocks_;
+    const std::size_t ndev = std::max<std::size_t>(1, device_.devices.size());
+    // A chunk is one kernel launch with one thread per message: long messages get larger
+    // chunks so that a launch still carries ~2^15 of them.
+    const std::uint64_t chunk_bytes =
+        std::min(kMaxChunkBytes, std::max(kChunkBytes, total / count_ * kChunkMinMessages));
+    std::size_t want = static_cast<std::size_t>((total + chunk_bytes - 1) / chunk_bytes);
+    want = std::min(ntasks_, std::max(want, ndev));
+    chunk_tasks_ = (ntasks_ + want - 1) / want;
+    nchunks_ = (ntasks_ + chunk_tasks_ - 1) / chunk_tasks_;
+    devices_used_ = static_cast<unsigned>(std::min(ndev, nchunks_));
+    threads_ = total < kPoolMinBytes ? 1u : static_cast<unsigned>(std::min<std::size_t>(workers_, ntasks_));
+    threads_ = std::max(threads_, devices_used_);
+
+    // Pinned staging is a ring of kRingChunks chunk buffers, not a copy of the batch: chunk k
+    // packs into buffer k mod ring once chunk k - ring has been unpacked.
+    ring_ = std::min(nchunks_, kRingChunks);
+    chunk_in_cap_ = chunk_out_cap_ = 0;
+    for (std::size_t k = 0; k < nchunks_; ++k) {
+      const std::size_t lo = chunk_first(k), hi = chunk_first(k + 1);
+      const std::uint64_t in = fixed_ ? (hi - lo) * first_len_ : chunk_base(k + 1) - chunk_base(k);
+      chunk_in_cap_ = std::max(chunk_in_cap_, (in + 63) & ~std::uint64_t{63});
+      chunk_out_cap_ = std::max(chunk_out_cap_, ((hi - lo) * digest_bytes_ + 63) & ~std::uint64_t{63});
+    }
+    const std::uint64_t fit = kRingBytes / std::max<std::uint64_t>(1, chunk_in_cap_ + chunk_out_cap_);
+    ring_ = std::max<std::size_t>(devices_used_, std::min<std::uint64_t>(ring_, fit));  // odd chunks: stay bounded
+    data_ = t_data_staging.reserve(std::max<std::uint64_t>(ring_ * chunk_in_cap_, 16));
+    packed_ = t_digest_staging.reserve(std::max<std::uint64_t>(ring_ * chunk_out_cap_, 16));
+    if (!fixed_) {  // filled by the pack tasks
+      offsets_.reset(new std::uint64_t[count_]);
+      lengths_.reset(new std::uint64_t[count_]);
+    }
+    next_pack_ = next_unpack_ = 0;
+    pack_left_.assign(nchunks_, 0);
+    for (std::size_t t = 0; t < ntasks_; ++t) pack_left_[t / chunk_tasks_] += 1;
+    unpack_left_ = pack_left_;
+    chunk_hashed_.assign(nchunks_, 0);
+    device_ms_.assign(devices_used_, 0.0);
+  }
+
+  void run_threads() {
+    std::vector<std::thread> pool;
+    pool.reserve(threads_ - 1);
+    for (unsigned t = 1; t < threads_; ++t) {
+      pool.emplace_back([this, t] { thread_main(t < devices_used_ ? static_cast<int>(t) : -1); });
+    }
+    thread_main(0);  // the caller drives the first device (batch.cpp:126)
+    for (auto& t : pool) t.join();
+  }
+
+  std::size_t task_first(std::size_t task) const {  // first message of a task
+    return std::min(count_, task * task_blocks_ * block_msgs_);
+  }
+  std::size_t chunk_first(std::size_t chunk) const {  // first message of a chunk
+    return task_first(std::min(ntasks_, chunk * chunk_tasks_));
+  }
+  std::uint64_t chunk_base(std::size_t chunk) const {  // ragged layout: first byte of a chunk
+    return block_base_[std::min(nblocks_, chunk * chunk_tasks_ * task_blocks_)];
+  }
+  std::uint8_t* chunk_in(std::size_t chunk) const { return data_ + (chunk % ring_) * chunk_in_cap_; }
+  std::uint8_t* chunk_out(std::size_t chunk) const { return packed_ + (chunk % ring_) * chunk_out_cap_; }
+
+  void pack_task(std::size_t task) {
+    const std::size_t lo = task_first(task), hi = task_first(task + 1);
+    const std::size_t chunk = task / chunk_tasks_;
+    if (fixed_) {
+      std::uint8_t* dst = chunk_in(chunk) + (lo - chunk_first(chunk)) * first_len_;
+      for (std::size_t i = lo; i < hi; ++i, dst += first_len_) {
+        const auto& m = batch_.messages[i];
+        if (m.size() != first_len_) {  // only a speculative plan can get here
+          mismatch_.store(true);
+          return;
+        }
+        if (first_len_) std::memcpy(dst, m.data(), first_len_);
+      }
+      return;
+    }
+    std::uint8_t* base = chunk_in(chunk);
+    std::uint64_t off = block_base_[task * task_blocks_] - chunk_base(chunk);  // within the chunk buffer
+    for (std::size_t i = lo; i < hi; ++i) {
+      const auto& m = batch_.messages[i];
+      offsets_[i] = off;
+      lengths_[i] = m.size();
+      if (!m.empty()) std::memcpy(base + off, m.data(), m.size());
+      off += pad8(m.size());
+    }
+  }
+
+  void unpack_task(std::size_t task) {
+    const std::size_t lo = task_first(task), hi = task_first(task + 1);
+    const std::size_t chunk = task / chunk_tasks_;
+    const std::uint8_t* d = chunk_out(chunk) + (lo - chunk_first(chunk)) * digest_bytes_;
+    for (std::size_t i = lo; i < hi; ++i, d += digest_bytes_) slots_[i].assign(d, d + digest_bytes_);
+  }
+
+  // One C-ABI call for the messages of chunk `chunk` on device slot `slot`.
+  void device_call(std::size_t chunk, int slot) {
+    const std::size_t first = chunk_first(chunk), n = chunk_first(chunk + 1) - first;
+    double ms = 0.0;
+    b200sha3_config cfg = make_config(device_, &ms);
+    if (!device_.devices.empty()) cfg.device = device_.devices[slot];
+    if (device_.devices.size() > 1) cfg.stream = nullptr;
+    std::uint8_t* out = chunk_out(chunk);
+    const int rc =
+        fixed_ ? b200sha3_hash_fixed(alg_, chunk_in(chunk), first_len_, n, batch_.xof_output_bits, out, &cfg)
+               : b200sha3_hash_batch(alg_, chunk_in(chunk), offsets_.get() + first, lengths_.get() + first,
+                                     n, batch_.xof_output_bits, out, &cfg);
+    if (rc == B200SHA3_ERR_INVALID_ARGUMENT) raise(rc);
+    if (rc != B200SHA3_OK) {
+      std::string where;
+      if (device_.devices.size() > 1) where = " on device " + std::to_string(device_.devices[slot]);
+      throw DeviceError(rc, std::string("b200sha3: ") + b200sha3_strerror(rc) + where + ": " +
+                                b200sha3_last_cuda_error());  // thread-local text: read it here
+    }
+    device_ms_[slot] += ms;  // only this slot's thread writes it
+  }
+
+  // Outer digest vector: `count` empty slots, 24 B each -- value-initialised by one thread
+  // (std::vector offers nothing else) and page-fault bound on fresh memory.  So: the storage
+  // is reserved once (transparent huge pages requested), which means growing the vector in
+  // steps never moves a slot; the other threads fault the pages of later steps in ahead of
+  // the builder (prefault_step); and after every step the slots built so far are published,
+  // so the unpack tasks below that mark run while the rest is still being built.  Stops early
+  // (to be resumed) when the pipeline is restarting.
+  void resize_result() {
+    if (result_.digests.capacity() < count_) {
+      result_.digests.reserve(count_);
+      advise_huge_pages(result_.digests.data(), count_ * sizeof(result_.digests[0]));
+      std::lock_guard<std::mutex> guard(mutex_);
+      slots_ = result_.digests.data();
+    }
+    for (std::size_t done = result_.digests.size(); done < count_ && !mismatch_.load();) {
+      const std::size_t step = done / kResizeStep;
+      std::uint8_t untouched = kStepUntouched;
+      if (!step_state_[step].compare_exchange_strong(untouched, kStepBuilt)) {
+        while (step_state_[step].load(std::memory_order_acquire) != kStepBuilt) std::this_thread::yield();
+      }
+      done = std::min(count_, (step + 1) * kResizeStep);
+      result_.digests.resize(done);
+      {
+        std::lock_guard<std::mutex> guard(mutex_);
+        slots_ready_ = done;
+      }
+      cv_.notify_all();
+    }
+  }
+
+  // Faults in the pages under the slots of one resize step that the builder has not reached.
+  // Only bytes of that step are written (zeros, into raw reserved storage), and the builder
+  // waits for a step being touched, so a slot is never written after it was constructed.
+  void prefault_step(std::size_t step) {
+    std::uint8_t untouched = kStepUntouched;
+    if (!step_state_[step].compare_exchange_strong(untouched, kStepTouching)) return;
+    auto* base = reinterpret_cast<volatile char*>(slots_);
+    const std::size_t lo = step * kResizeStep * sizeof(result_.digests[0]);
+    const std::size_t hi = std::min(count_, (step + 1) * kResizeStep) * sizeof(result_.digests[0]);
+    for (std::size_t b = lo; b < hi; b += 4096) base[b] = 0;
+    step_state_[step].store(kStepBuilt, std::memory_order_release);
+  }
+
+  // Runs f() with the scheduler lock released; a throw marks the pipeline failed (the first
+  // exception is kept, the other threads drain; batch.cpp:95-117).  Returns the seconds f took.
+  template <class F>
+  double unlocked(std::unique_lock<std::mutex>& lock, F f) {
+    lock.unlock();
+    const auto t0 = clock::now();
+    try {
+      f();
+    } catch (...) {
+      lock.lock();
+      if (!failed_) {
+        failed_ = true;
+        error_ = std::current_exception();
+      }
+      cv_.notify_all();
+      return since(t0);
+    }
+    const double s = since(t0);
+    lock.lock();
+    return s;
+  }
+
+  bool ring_slot_free(std::size_t chunk) const {  // under mutex_
+    return chunk < ring_ || unpack_left_[chunk - ring_] == 0;
+  }
+
+  // slot >= 0: this thread also issues the device calls of chunks slot, slot + n, ...
+  void thread_main(int slot) {
+    std::unique_lock<std::mutex> lock(mutex_);
+    std::size_t my_chunk = slot >= 0 ? static_cast<std::size_t>(slot) : nchunks_;
+    for (;;) {
+      if (failed_ || mismatch_.load()) {
+        cv_.notify_all();
+        return;
+      }
+      if (my_chunk < nchunks_ && pack_left_[my_chunk] == 0) {
+        const std::size_t k = my_chunk;
+        device_calls_s_ += unlocked(lock, [&] { device_call(k, slot); });
+        chunk_hashed_[k] = 1;
+        my_chunk += devices_used_;
+        cv_.notify_all();
+      } else if (!resize_taken_ && slots_ready_ < count_ &&
+                 (slot < 0 || threads_ == devices_used_)) {  // a pure worker, if there is one
+        resize_taken_ = true;
+        resize_s_ += unlocked(lock, [&] { resize_result(); });
+        resize_taken_ = false;
+        cv_.notify_all();
+      } else if (slots_ && next_prefault_ < nsteps_) {
+        const std::size_t step = next_prefault_++;
+        unlocked(lock, [&] { prefault_step(step); });
+      } else if (next_pack_ < ntasks_ && ring_slot_free(next_pack_ / chunk_tasks_)) {
+        const std::size_t t = next_pack_++;
+        pack_cpu_s_ += unlocked(lock, [&] { pack_task(t); });
+        if (--pack_left_[t / chunk_tasks_] == 0) cv_.notify_all();
+      } else if (next_unpack_ < ntasks_ && task_first(next_unpack_ + 1) <= slots_ready_ &&
+                 chunk_hashed_[next_unpack_ / chunk_tasks_]) {
+        const std::size_t t = next_unpack_++;
+        unpack_cpu_s_ += unlocked(lock, [&] { unpack_task(t); });
+        if (--unpack_left_[t / chunk_tasks_] == 0) cv_.notify_all();  // its ring buffers are free
+      } else if (next_unpack_ == ntasks_ && my_chunk >= nchunks_) {
+        return;  // nothing left to take; tasks still running finish before the join
+      } else {
+        cv_.wait(lock);
+      }
+    }
+  }
+
+  const HashBatch& batch_;
+  const DeviceConfig& device_;
+  const int alg_;
+  const std::uint64_t digest_bytes_;
+  const unsigned workers_;
+  BatchResult& result_;
+  const std::size_t count_;
+
+  // plan
+  std::size_t block_msgs_ = 1, nblocks_ = 0, task_blocks_ = 1, ntasks_ = 0, chunk_tasks_ = 1, nchunks_ = 0;
+  std::unique_ptr<std::uint64_t[]> block_base_, offsets_, lengths_;
+  std::uint64_t first_len_ = 0, total_in_ = 0;
+  bool fixed_ = true, speculative_ = false;
+  unsigned threads_ = 1, devices_used_ = 1;
+  std::size_t ring_ = 1;
+  std::uint64_t chunk_in_cap_ = 0, chunk_out_cap_ = 0;
+  std::uint8_t* data_ = nullptr;    // ring_ x chunk_in_cap_ bytes, pinned
+  std::uint8_t* packed_ = nullptr;  // ring_ x chunk_out_cap_ bytes, pinned
+
+  // scheduler state, under mutex_
+  std::mutex mutex_;
+  std::condition_variable cv_;
+  std::size_t next_pack_ = 0, next_unpack_ = 0, slots_ready_ = 0, next_prefault_ = 1, nsteps_ = 0;
+  std::unique_ptr<std::atomic<std::uint8_t>[]> step_state_;
+  std::vector<std::uint8_t>* slots_ = nullptr;
+  std::vector<std::size_t> pack_left_, unpack_left_;
+  std::vector<char> chunk_hashed_;
+  bool resize_taken_ = false, failed_ = false;
+  std::atomic<bool> mismatch_{false};
+  std::exception_ptr error_;
+  std::vector<double> device_ms_;
+  double resize_s_ = 0, device_calls_s_ = 0, pack_cpu_s_ = 0, unpack_cpu_s_ = 0;
+};
+
 BatchResult hash_batch(const HashBatch& batch, const EngineConfig& config,
                        const DeviceConfig& device) {
   const int alg = static_cast<int>(batch.algorithm);
@@ -139,107 +555,9 @@ BatchResult hash_batch(const HashBatch& batch, const EngineConfig& config,
   if (alg < 0 || alg > 5) throw std::invalid_argument("hash_batch: unknown algorithm");
   if (is_xof && batch.xof_output_bits == 0) raise(B200SHA3_ERR_INVALID_ARGUMENT);
 
-  const std::size_t count = batch.messages.size();
-  const std::uint64_t digest_bytes = b200sha3_digest_bytes(alg, batch.xof_output_bits);
   BatchResult result;
-  result.digests.resize(count);
-  if (count == 0) return result;  // test_batch.cpp:113-117
-  const unsigned workers = pack_workers(config);
-
-  // Pack.  Equal-length batches (what generate_workload builds, workload.cpp:34-45) go back
-  // to back and take the fixed-length entry: no offset table, no bucketing pass, one launch.
-  // Ragged batches get 8-byte aligned offsets so the device can use aligned 64-bit loads.
-  std::vector<std::uint64_t> offsets(count), lengths(count);
-  const std::uint64_t first_len = batch.messages[0].size();
-  bool fixed = true;
-  for (std::size_t i = 0; i < count; ++i) {
-    lengths[i] = batch.messages[i].size();
-    fixed = fixed && lengths[i] == first_len;
-  }
-  std::uint64_t total = 0;
-  for (std::size_t i = 0; i < count; ++i) {
-    offsets[i] = total;
-    total += fixed ? first_len : ((lengths[i] + 7) & ~std::uint64_t{7});
-  }
-  std::uint8_t* data = t_data_staging.reserve(std::max<std::uint64_t>(total, 16));
-  parallel_ranges(count, workers, total, [&](std::size_t begin, std::size_t end) {
-    for (std::size_t i = begin; i < end; ++i) {
-      if (lengths[i]) std::memcpy(data + offsets[i], batch.messages[i].data(), lengths[i]);
-    }
-  });
-
-  std::uint8_t* packed = t_digest_staging.reserve(std::max<std::uint64_t>(count * digest_bytes, 16));
-  double ms = 0.0;
-  int rc = B200SHA3_OK;
-  if (device.devices.size() <= 1) {
-    b200sha3_config cfg = make_config(device, &ms);
-    if (device.devices.size() == 1) cfg.device = device.devices[0];
-    rc = fixed ? b200sha3_hash_fixed(alg, data, first_len, count, batch.xof_output_bits, packed, &cfg)
-               : b200sha3_hash_batch(alg, data, offsets.data(), lengths.data(), count,
-                                     batch.xof_output_bits, packed, &cfg);
-  } else {
-    // One contiguous range per device, cut at equal cumulative permutation counts.
-    const std::size_t ndev = device.devices.size();
-    const std::uint64_t rate = b200sha3_rate_bytes(alg);
-    std::uint64_t work = 0;
-    for (std::size_t i = 0; i < count; ++i) work += lengths[i] / rate + 1;
-    std::vector<std::size_t> cut(ndev + 1, count);
-    cut[0] = 0;
-    std::uint64_t acc = 0;
-    std::size_t next = 1;
-    for (std::size_t i = 0; i < count && next < ndev; ++i) {
-      while (next < ndev && acc >= work * next / ndev) cut[next++] = i;
-      acc += lengths[i] / rate + 1;
-    }
-    std::vector<int> status(ndev, B200SHA3_OK);
-    std::vector<double> dev_ms(ndev, 0.0);
-    std::vector<std::string> errors(ndev);
-    auto run = [&](std::size_t k) {
-      const std::size_t b = cut[k], e = cut[k + 1];
-      if (e <= b) return;
-      b200sha3_config cfg = make_config(device, &dev_ms[k]);
-      cfg.device = device.devices[k];
-      cfg.stream = nullptr;
-      status[k] = fixed ? b200sha3_hash_fixed(alg, data + b * first_len, first_len, e - b,
-                                              batch.xof_output_bits, packed + b * digest_bytes, &cfg)
-                        : b200sha3_hash_batch(alg, data, offsets.data() + b, lengths.data() + b, e - b,
-                                              batch.xof_output_bits, packed + b * digest_bytes, &cfg);
-      if (status[k] != B200SHA3_OK) errors[k] = b200sha3_last_cuda_error();  // thread-local text
-    };
-    {
-      std::vector<std::thread> pool;
-      for (std::size_t k = 1; k < ndev; ++k) pool.emplace_back(run, k);
-      run(0);  // the caller drives the first device (batch.cpp:126)
-      for (auto& t : pool) t.join();
-    }
-    for (std::size_t k = 0; k < ndev; ++k) {
-      ms = std::max(ms, dev_ms[k]);
-      if (status[k] != B200SHA3_OK && rc == B200SHA3_OK) {  // first failure wins (batch.cpp:111-117)
-        rc = status[k];
-        if (rc != B200SHA3_ERR_INVALID_ARGUMENT) {
-          t_data_staging.trim(0);
-          t_digest_staging.trim(0);
-          throw DeviceError(rc, std::string("b200sha3: ") + b200sha3_strerror(rc) + " on device " +
-                                    std::to_string(device.devices[k]) + ": " + errors[k]);
-        }
-      }
-    }
-  }
-  if (rc != B200SHA3_OK) {
-    t_data_staging.trim(0);
-    t_digest_staging.trim(0);
-    raise(rc);
-  }
-
-  parallel_ranges(count, workers, count * digest_bytes, [&](std::size_t begin, std::size_t end) {
-    for (std::size_t i = begin; i < end; ++i) {
-      const std::uint8_t* d = packed + i * digest_bytes;
-      result.digests[i].assign(d, d + digest_bytes);
-    }
-  });
-  t_data_staging.trim(kKeepBytes);
-  t_digest_staging.trim(kKeepBytes);
-  result.elapsed = std::chrono::duration<double>(ms * 1e-3);
+  if (batch.messages.empty()) return result;  // test_batch.cpp:113-117
+  BatchPipeline(batch, config, device, b200sha3_digest_bytes(alg, batch.xof_output_bits), result).run();
   return result;
 }
 

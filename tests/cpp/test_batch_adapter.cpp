@@ -7,6 +7,7 @@
 //
 //   test_batch_adapter            all cases (needs a GPU)
 //   test_batch_adapter --cpu-only the cases that must work without a device
+#include <algorithm>
 #include <array>
 #include <cstdio>
 #include <cstring>
@@ -222,6 +223,46 @@ void gpu_cases() {
       ok = res.digests[i] == expect(batch.algorithm, batch.messages[i]);
     }
     CHECK(ok);
+  }
+  {  // a large batch that LOOKS equal-length (every sampled size agrees) but is not: the
+     // adapter starts on the fixed-length layout, a pack task finds the odd message and the
+     // call restarts on the ragged layout.  Also the all-empty batch (length 0 everywhere).
+    Rng rng(78);
+    HashBatch batch;
+    const std::size_t count = (1u << 18) + 4321;
+    batch.messages.resize(count);
+    for (auto& m : batch.messages) {
+      m.resize(24);
+      for (std::size_t i = 0; i < 24; i += 8) {
+        const std::uint64_t w = rng.next();
+        std::memcpy(m.data() + i, &w, 8);
+      }
+    }
+    for (const std::size_t odd : {count / 2 + 3, count - 2}) {
+      HashBatch ragged = batch;
+      ragged.messages[odd].resize(odd % 2 ? 200 : 0, 0x5a);
+      b200::StageTimes st;
+      b200::DeviceConfig dev;
+      dev.stages = &st;
+      const BatchResult res = b200::hash_batch(ragged, {}, dev);
+      bool ok = res.digests.size() == count;
+      for (std::size_t i = 0; ok && i < count; i += 1009) {
+        ok = res.digests[i] == expect(ragged.algorithm, ragged.messages[i]);
+      }
+      for (std::size_t i = odd - 2; ok && i < std::min(count, odd + 3); ++i) {
+        ok = res.digests[i] == expect(ragged.algorithm, ragged.messages[i]);
+      }
+      CHECK(ok);
+      CHECK(st.threads >= 1 && st.chunks >= 1);
+    }
+    HashBatch empties;
+    empties.algorithm = Algorithm::sha3_512;
+    empties.messages.resize(count);
+    const BatchResult res = hash_batch(empties, {});
+    const auto e = expect(Algorithm::sha3_512, {});
+    bool ok = res.digests.size() == count;
+    for (std::size_t i = 0; ok && i < count; i += 511) ok = res.digests[i] == e;
+    CHECK(ok && res.digests.back() == e);
   }
   {  // several devices: contiguous ranges of equal work, one host thread each.  The box has
      // one GPU, so the same ordinal is listed three times -- the sharding, threading and
