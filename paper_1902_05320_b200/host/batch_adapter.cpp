@@ -229,15 +229,22 @@ class BatchPipeline {
   }
   static std::uint64_t pad8(std::uint64_t n) { return (n + 7) & ~std::uint64_t{7}; }
 
-  static constexpr std::uint64_t kTaskBytes = 1ull << 20;      // input + output per task
-  static constexpr std::uint64_t kChunkBytes = 32ull << 20;    // input + output per device call ...
-  static constexpr std::uint64_t kChunkMinMessages = 1u << 15; // ... grown to hold this many messages
-  static constexpr std::uint64_t kMaxChunkBytes = 1ull << 30;  // ... up to this
-  static constexpr std::uint64_t kPoolMinBytes = 4ull << 20;   // below: the caller works alone
-  static constexpr std::size_t kParallelScanMin = 1u << 18;    // messages
-  static constexpr std::size_t kRingChunks = 12;               // pinned staging: chunks in flight
-  static constexpr std::uint64_t kRingBytes = 1ull << 30;      // ... and their bytes, at most
-  static constexpr std::size_t kResizeStep = 1u << 17;         // digest slots per published step
+  // Plan granularity.  The sanitizer build of tests/cpp shrinks it (-DB200SHA3_ADAPTER_TEST_SCALE=n
+  // divides every size by 2^n) so that ring wrap-around, multi-step resizes, the parallel scan and
+  // the speculative restart all happen on batches small enough for a CPU test.
+#ifndef B200SHA3_ADAPTER_TEST_SCALE
+#define B200SHA3_ADAPTER_TEST_SCALE 0
+#endif
+  static constexpr int kScale = B200SHA3_ADAPTER_TEST_SCALE;
+  static constexpr std::uint64_t kTaskBytes = (1ull << 20) >> kScale;     // input + output per task
+  static constexpr std::uint64_t kChunkBytes = (32ull << 20) >> kScale;   // input + output per device call ...
+  static constexpr std::uint64_t kChunkMinMessages = (1u << 15) >> kScale;  // ... grown to hold this many messages
+  static constexpr std::uint64_t kMaxChunkBytes = (1ull << 30) >> kScale;   // ... up to this
+  static constexpr std::uint64_t kPoolMinBytes = (4ull << 20) >> kScale;  // below: the caller works alone
+  static constexpr std::size_t kParallelScanMin = (1u << 18) >> kScale;   // messages
+  static constexpr std::size_t kRingChunks = 12;                          // pinned staging: chunks in flight
+  static constexpr std::uint64_t kRingBytes = (1ull << 30) >> kScale;     // ... and their bytes, at most
+  static constexpr std::size_t kResizeStep = (1u << 17) >> kScale;        // digest slots per published step
   static constexpr std::uint8_t kStepUntouched = 0, kStepTouching = 1, kStepBuilt = 2;
 
   bool sample_is_fixed() const {
