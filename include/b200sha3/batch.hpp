@@ -92,8 +92,8 @@ struct DeviceConfig {
   void* stream = nullptr;    // cudaStream_t
   std::uint32_t flags = 0;   // B200SHA3_FLAG_*
   int kernel = 0;            // B200SHA3_KERNEL_*
-  // More than one entry: the batch is cut into contiguous message ranges of equal work
-  // (Keccak-f permutations), one per listed device, each driven by its own host thread --
+  // More than one entry: the chunks of the call's pipeline (contiguous message ranges) are
+  // dealt round-robin to the listed devices, each driven by its own host thread --
   // plan_partition (batch.cpp:46-62) one level up; no inter-device traffic, digests land
   // in message order.  `device` and `stream` are then ignored.
   std::vector<int> devices;

@@ -299,7 +299,7 @@ class BatchPipeline {
     // chunks so that a launch still carries ~2^15 of them.
     const std::uint64_t chunk_bytes =
         std::min(kMaxChunkBytes, std::max(kChunkBytes, total / count_ * kChunkMinMessages));
-    std::size_t want = static_cast<std::size_t>((total + chunk_bytes - 1) / chunk_bytes);
+    std::size_t want = static_cast<std::size_t>((total + chunk_bytes / 2) / chunk_bytes);  // nearest
     want = std::min(ntasks_, std::max(want, ndev));
     chunk_tasks_ = (ntasks_ + want - 1) / want;
     nchunks_ = (ntasks_ + chunk_tasks_ - 1) / chunk_tasks_;

@@ -264,7 +264,7 @@ void gpu_cases() {
     for (std::size_t i = 0; ok && i < count; i += 511) ok = res.digests[i] == e;
     CHECK(ok && res.digests.back() == e);
   }
-  {  // several devices: contiguous ranges of equal work, one host thread each.  The box has
+  {  // several devices: chunks dealt round-robin, one host thread per device.  The box has
      // one GPU, so the same ordinal is listed three times -- the sharding, threading and
      // in-order digest placement are what is under test.
     Rng rng(91);
