@@ -2,7 +2,12 @@
 // chunked copy / compute pipelines over the device paths of capi.cu, and the pinned
 // staging allocator.
 #include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -160,6 +165,261 @@ class SlotPipeline {
   double kernel_ms_ = 0.0;
 };
 
+
+// ---- pageable host memory ----------------------------------------------------------------
+// cudaMemcpyAsync on pageable memory is staged by the driver through one thread: 8-10 GB/s
+// measured on the B200 boxes against 50-55 GB/s from pinned memory, and synchronous.  A caller
+// of the C ABI that holds its batch in ordinary malloc/std::vector memory (INTEGRATION.md,
+// binding 1) would spend 5x longer in copies than the link needs.  So the host entries stage
+// pageable buffers themselves: helper threads memcpy 8 MiB blocks into a small ring of pinned
+// bounce buffers (cached per calling thread) and the copy engines take it from there; digests
+// come back the same way.  Pinned callers (b200sha3_pinned_alloc, cudaHostRegister) skip all this.
+
+bool is_pageable(const void* p) {
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return attr.type == cudaMemoryTypeUnregistered;
+}
+
+// Helper threads that live for one call; copy() is a parallel memcpy that returns when done.
+class CopyPool {
+ public:
+  explicit CopyPool(unsigned helpers) {
+    for (unsigned i = 0; i < helpers; ++i) threads_.emplace_back([this, i] { worker(i + 1); });
+  }
+  CopyPool(const CopyPool&) = delete;
+  CopyPool& operator=(const CopyPool&) = delete;
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++generation_;
+    }
+    wake_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+
+  void copy(void* dst, const void* src, size_t bytes) {
+    if (threads_.empty() || bytes < (1u << 20)) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(m_);
+      dst_ = static_cast<uint8_t*>(dst);
+      src_ = static_cast<const uint8_t*>(src);
+      bytes_ = bytes;
+      const size_t parts = threads_.size() + 1;
+      piece_ = ((bytes + parts - 1) / parts + 4095) & ~size_t{4095};
+      pending_ = threads_.size();
+      ++generation_;
+    }
+    wake_.notify_all();
+    copy_piece(0);
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void copy_piece(size_t index) {
+    const size_t lo = std::min(bytes_, index * piece_), hi = std::min(bytes_, lo + piece_);
+    if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+  }
+  void worker(size_t index) {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(m_);
+    for (;;) {
+      wake_.wait(lk, [&] { return generation_ != seen; });
+      seen = generation_;
+      if (stop_) return;
+      lk.unlock();
+      copy_piece(index);
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+
+  std::vector<std::thread> threads_;
+  std::mutex m_;
+  std::condition_variable wake_, done_;
+  uint64_t generation_ = 0;
+  bool stop_ = false;
+  uint8_t* dst_ = nullptr;
+  const uint8_t* src_ = nullptr;
+  size_t bytes_ = 0, piece_ = 0, pending_ = 0;
+};
+
+// The pinned bounce ring of one calling thread: kSlots blocks of kBlock bytes, used round-robin
+// by both directions.  A slot is reused once the copy engine is done with it (its event) and,
+// for a digest block, once it has been copied out to the caller's buffer.
+class BounceRing {
+ public:
+  static constexpr size_t kBlock = 8u << 20;
+  static constexpr int kSlots = 8;
+
+  ~BounceRing() {
+    for (cudaEvent_t e : events_) {
+      if (e) cudaEventDestroy(e);
+    }
+    if (base_) cudaFreeHost(base_);
+  }
+
+  cudaError_t init() {
+    if (base_) return cudaSuccess;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&base_), kBlock * kSlots, cudaHostAllocPortable);
+    for (int i = 0; e == cudaSuccess && i < kSlots; ++i) {
+      e = cudaEventCreateWithFlags(&events_[i], cudaEventDisableTiming);
+    }
+    return e;
+  }
+
+  // dst (device) <- src (pageable host), asynchronous on `stream` once the bytes are staged.
+  cudaError_t h2d(void* dst, const void* src, size_t bytes, cudaStream_t stream, CopyPool& pool) {
+    for (size_t off = 0; off < bytes; off += kBlock) {
+      const size_t n = std::min(kBlock, bytes - off);
+      int slot = 0;
+      cudaError_t e = acquire(&slot, pool);
+      if (e != cudaSuccess) return e;
+      pool.copy(block(slot), static_cast<const uint8_t*>(src) + off, n);
+      e = cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, block(slot), n, cudaMemcpyHostToDevice, stream);
+      if (e == cudaSuccess) e = cudaEventRecord(events_[slot], stream);
+      if (e != cudaSuccess) return e;
+      busy_[slot] = true;
+    }
+    return cudaSuccess;
+  }
+
+  // dst (pageable host) <- src (device): the DMA into the ring is enqueued now, the copy out to
+  // `dst` happens when the slot comes round again or at flush().
+  cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t stream, CopyPool& pool) {
+    for (size_t off = 0; off < bytes; off += kBlock) {
+      const size_t n = std::min(kBlock, bytes - off);
+      int slot = 0;
+      cudaError_t e = acquire(&slot, pool);
+      if (e != cudaSuccess) return e;
+      e = cudaMemcpyAsync(block(slot), static_cast<const uint8_t*>(src) + off, n, cudaMemcpyDeviceToHost, stream);
+      if (e == cudaSuccess) e = cudaEventRecord(events_[slot], stream);
+      if (e != cudaSuccess) return e;
+      busy_[slot] = true;
+      out_dst_[slot] = static_cast<uint8_t*>(dst) + off;
+      out_bytes_[slot] = n;
+    }
+    return cudaSuccess;
+  }
+
+  // Waits for every slot and delivers the digest blocks still in the ring.
+  cudaError_t flush(CopyPool& pool) {
+    cudaError_t first = cudaSuccess;
+    for (int i = 0; i < kSlots; ++i) {
+      const cudaError_t e = release((next_ + i) % kSlots, pool);
+      if (e != cudaSuccess && first == cudaSuccess) first = e;
+    }
+    return first;
+  }
+
+  // After a failed call: forget what was in flight (the streams have been synchronised).
+  void abandon() {
+    for (int i = 0; i < kSlots; ++i) {
+      busy_[i] = false;
+      out_bytes_[i] = 0;
+    }
+  }
+
+ private:
+  uint8_t* block(int slot) const { return base_ + static_cast<size_t>(slot) * kBlock; }
+  cudaError_t release(int slot, CopyPool& pool) {
+    if (!busy_[slot]) return cudaSuccess;
+    const cudaError_t e = cudaEventSynchronize(events_[slot]);
+    if (e == cudaSuccess && out_bytes_[slot]) pool.copy(out_dst_[slot], block(slot), out_bytes_[slot]);
+    busy_[slot] = false;
+    out_bytes_[slot] = 0;
+    return e;
+  }
+  cudaError_t acquire(int* slot, CopyPool& pool) {
+    *slot = next_;
+    next_ = (next_ + 1) % kSlots;
+    return release(*slot, pool);
+  }
+
+  uint8_t* base_ = nullptr;
+  cudaEvent_t events_[kSlots] = {};
+  bool busy_[kSlots] = {};
+  uint8_t* out_dst_[kSlots] = {};
+  size_t out_bytes_[kSlots] = {};
+  int next_ = 0;
+};
+
+struct BounceCache {  // one ring per (calling thread, device): pinned memory is per context
+  std::vector<std::unique_ptr<BounceRing>> per_device;
+};
+thread_local BounceCache t_bounce;
+
+// Host <-> device copies of one call: straight cudaMemcpyAsync for pinned memory, through the
+// bounce ring for pageable memory that is large enough to matter.
+class HostIo {
+ public:
+  static constexpr uint64_t kBounceMinBytes = 4u << 20;
+
+  // `*_bytes`: what the call will move in total per buffer (decides whether staging pays).
+  // `meta` is the offset / length tables of the variable-length entry (one allocation or two:
+  // the first one's kind is taken for both).
+  cudaError_t init(const void* in, uint64_t in_bytes, const void* out, uint64_t out_bytes,
+                   const void* meta = nullptr, uint64_t meta_bytes = 0) {
+    static const bool disabled = std::getenv("B200SHA3_NO_BOUNCE") != nullptr;
+    bounce_in_ = !disabled && in && in_bytes >= kBounceMinBytes && is_pageable(in);
+    bounce_out_ = !disabled && out && out_bytes >= kBounceMinBytes && is_pageable(out);
+    bounce_meta_ = !disabled && meta && meta_bytes >= kBounceMinBytes && is_pageable(meta);
+    if (!bounce_in_ && !bounce_out_ && !bounce_meta_) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= static_cast<int>(t_bounce.per_device.size())) t_bounce.per_device.resize(dev + 1);
+    if (!t_bounce.per_device[dev]) t_bounce.per_device[dev] = std::make_unique<BounceRing>();
+    ring_ = t_bounce.per_device[dev].get();
+    e = ring_->init();
+    if (e != cudaSuccess) {  // no pinned memory to be had: fall back to the driver's staging
+      cudaGetLastError();
+      t_bounce.per_device[dev].reset();
+      ring_ = nullptr;
+      bounce_in_ = bounce_out_ = bounce_meta_ = false;
+      return cudaSuccess;
+    }
+    const unsigned hw = std::thread::hardware_concurrency();  // helpers + the caller: half the cores, <= 8
+    pool_ = std::make_unique<CopyPool>(hw >= 4 ? std::min(7u, hw / 2 - 1) : 0u);
+    return cudaSuccess;
+  }
+
+  cudaError_t h2d(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+    if (!bounce_in_) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream);
+    return ring_->h2d(dst, src, bytes, stream, *pool_);
+  }
+  cudaError_t h2d_meta(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+    if (!bounce_meta_) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream);
+    return ring_->h2d(dst, src, bytes, stream, *pool_);
+  }
+  cudaError_t d2h(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+    if (!bounce_out_) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream);
+    return ring_->d2h(dst, src, bytes, stream, *pool_);
+  }
+  // After the streams have drained: deliver what is still in the ring.
+  cudaError_t finish(bool ok) {
+    if (!ring_) return cudaSuccess;
+    if (!ok) {
+      ring_->abandon();
+      return cudaSuccess;
+    }
+    return ring_->flush(*pool_);
+  }
+
+ private:
+  bool bounce_in_ = false, bounce_out_ = false, bounce_meta_ = false;
+  BounceRing* ring_ = nullptr;
+  std::unique_ptr<CopyPool> pool_;
+};
+
 struct HostChunk {
   uint64_t first, count;  // message range
   uint64_t lo, hi;        // byte range of `data` the chunk reads (lo is 16-byte aligned)
@@ -202,10 +462,12 @@ HostChunk whole_batch_chunk(const uint64_t* offsets, const uint64_t* lengths, ui
   return HostChunk{0, count, lo & ~15ull, hi};  // device copy congruent to the host buffer mod 16
 }
 
-int finish_call(int rc, SlotPipeline& pipe, const Config& c, uint32_t launches) {
+int finish_call(int rc, SlotPipeline& pipe, HostIo& io, const Config& c, uint32_t launches) {
   double kernel_ms = 0.0;
-  const cudaError_t e = pipe.drain(&kernel_ms);
+  cudaError_t e = pipe.drain(&kernel_ms);
   if (rc == B200SHA3_OK && e != cudaSuccess) rc = cuda_fail(e, "pipeline drain");
+  e = io.finish(rc == B200SHA3_OK);
+  if (rc == B200SHA3_OK && e != cudaSuccess) rc = cuda_fail(e, "digest delivery");
   if (rc != B200SHA3_OK) {
     cudaGetLastError();
     return rc;
@@ -241,6 +503,8 @@ int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_t msg_len, ui
   chunk = std::min(std::max<uint64_t>(chunk, 16), count);
   SlotPipeline pipe(chunk < count ? kPipelineSlots : 1, c.device_ms != nullptr);
   CU(pipe.init());
+  HostIo io;
+  CU(io.init(data, count * msg_len, digests, count * digest_bytes));
   uint8_t* d_in[kPipelineSlots] = {};
   uint8_t* d_out[kPipelineSlots] = {};
   for (int s = 0; s < pipe.slots(); ++s) {
@@ -255,8 +519,7 @@ int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_t msg_len, ui
     const uint64_t n = std::min(chunk, count - done);
     cudaError_t e = cudaSuccess;
     if (msg_len) {
-      e = cudaMemcpyAsync(d_in[s], data + done * msg_len, n * msg_len, cudaMemcpyHostToDevice,
-                          pipe.stream(s));
+      e = io.h2d(d_in[s], data + done * msg_len, n * msg_len, pipe.stream(s));
     }
     if (e == cudaSuccess) e = pipe.begin_kernels(s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D copy"); break; }
@@ -265,13 +528,12 @@ int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_t msg_len, ui
     if (rc != B200SHA3_OK) break;
     e = pipe.end_kernels(s);
     if (e == cudaSuccess) {
-      e = cudaMemcpyAsync(digests + done * digest_bytes, d_out[s], n * digest_bytes,
-                          cudaMemcpyDeviceToHost, pipe.stream(s));
+      e = io.d2h(digests + done * digest_bytes, d_out[s], n * digest_bytes, pipe.stream(s));
     }
     if (e != cudaSuccess) { rc = cuda_fail(e, "D2H copy"); break; }
     done += n;
   }
-  return finish_call(rc, pipe, c, launches);
+  return finish_call(rc, pipe, io, c, launches);
 }
 
 // Host entry, variable-length messages.  A packed batch is cut into chunks of ~64 MiB of
@@ -309,6 +571,10 @@ int b200sha3_hash_batch(int algorithm, const uint8_t* data, const uint64_t* offs
   SlotPipeline pipe(static_cast<int>(std::min<size_t>(kPipelineSlots, chunks.size())),
                     c.device_ms != nullptr);
   CU(pipe.init());
+  uint64_t total_span = 0;
+  for (const HostChunk& ch : chunks) total_span += ch.hi - ch.lo;
+  HostIo io;
+  CU(io.init(data, total_span, digests, count * digest_bytes, offsets, 2 * count * sizeof(uint64_t)));
   uint8_t* d_data[kPipelineSlots] = {};
   uint64_t* d_meta[kPipelineSlots] = {};  // offsets, then lengths
   uint8_t* d_out[kPipelineSlots] = {};
@@ -325,15 +591,13 @@ int b200sha3_hash_batch(int algorithm, const uint8_t* data, const uint64_t* offs
     cudaStream_t stream = pipe.stream(s);
     cudaError_t e = cudaSuccess;
     if (ch.hi > ch.lo) {
-      e = cudaMemcpyAsync(d_data[s], data + ch.lo, ch.hi - ch.lo, cudaMemcpyHostToDevice, stream);
+      e = io.h2d(d_data[s], data + ch.lo, ch.hi - ch.lo, stream);
     }
     if (e == cudaSuccess) {
-      e = cudaMemcpyAsync(d_meta[s], offsets + ch.first, ch.count * sizeof(uint64_t),
-                          cudaMemcpyHostToDevice, stream);
+      e = io.h2d_meta(d_meta[s], offsets + ch.first, ch.count * sizeof(uint64_t), stream);
     }
     if (e == cudaSuccess) {
-      e = cudaMemcpyAsync(d_meta[s] + max_count, lengths + ch.first, ch.count * sizeof(uint64_t),
-                          cudaMemcpyHostToDevice, stream);
+      e = io.h2d_meta(d_meta[s] + max_count, lengths + ch.first, ch.count * sizeof(uint64_t), stream);
     }
     if (e == cudaSuccess) e = pipe.begin_kernels(s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D copy"); break; }
@@ -343,12 +607,11 @@ int b200sha3_hash_batch(int algorithm, const uint8_t* data, const uint64_t* offs
     if (rc != B200SHA3_OK) break;
     e = pipe.end_kernels(s);
     if (e == cudaSuccess) {
-      e = cudaMemcpyAsync(digests + ch.first * digest_bytes, d_out[s], ch.count * digest_bytes,
-                          cudaMemcpyDeviceToHost, stream);
+      e = io.d2h(digests + ch.first * digest_bytes, d_out[s], ch.count * digest_bytes, stream);
     }
     if (e != cudaSuccess) { rc = cuda_fail(e, "D2H copy"); break; }
   }
-  return finish_call(rc, pipe, c, launches);
+  return finish_call(rc, pipe, io, c, launches);
 }
 
 // Page-locked host memory for callers that want the copy/compute pipeline at full PCIe

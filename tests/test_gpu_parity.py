@@ -521,3 +521,35 @@ def test_pinned_alloc_api(engine):
     assert out.tobytes() == hashlib.sha3_256(bytes(range(64))).digest()
     assert lib.b200sha3_pinned_free(p) == 0
     assert lib.b200sha3_pinned_alloc(0, C.byref(p)) == 0 and not p.value
+
+
+def test_pageable_host_buffers_are_staged_through_the_bounce_ring(engine, oracle):
+    """Host entries on ordinary (pageable) memory >= 4 MiB stage blocks through pinned bounce
+    buffers with helper threads (csrc/capi_host.cu, BounceRing): every mix of pageable / pinned
+    input and output, and a ragged batch whose offset / length tables are large enough to be
+    staged too, must give the digests of the device-buffer entry."""
+    import torch
+    count = 700_001                     # 42.7 MiB in, 21.4 MiB out: several 8 MiB blocks, ragged tail
+    dev = engine.generate_workload(count * 64, 64, seed=9, count=count)
+    want = engine.hash_fixed("sha3_256", dev, 64, count).cpu().numpy()
+    pageable_in = dev.cpu().numpy().copy()
+    pinned_in = torch.from_numpy(pageable_in).pin_memory()
+    for src in (pageable_in.ctypes.data, pinned_in.data_ptr()):
+        pageable_out = np.zeros((count, 32), dtype=np.uint8)
+        pinned_out = torch.zeros((count, 32), dtype=torch.uint8).pin_memory()
+        engine.hash_fixed_ptr("sha3_256", src, 64, count, pageable_out.ctypes.data)
+        engine.hash_fixed_ptr("sha3_256", src, 64, count, pinned_out.data_ptr())
+        assert (pageable_out == want).all() and (pinned_out.numpy() == want).all()
+
+    rng = np.random.default_rng(21)
+    count = 400_000                     # 6.4 MB of offsets + lengths
+    lengths = rng.integers(0, 200, count).astype(np.uint64)
+    offsets = (np.cumsum(lengths) - lengths).astype(np.uint64)        # unaligned starts
+    data = rng.integers(0, 256, int(lengths.sum()) + 16, dtype=np.uint8)
+    host = engine.hash_batch("shake256", data, offsets, lengths, 264)
+    on_device = engine.hash_batch("shake256", torch.from_numpy(data).cuda(), torch.from_numpy(offsets).cuda(),
+                                  torch.from_numpy(lengths).cuda(), 264).cpu().numpy()
+    assert (host == on_device).all()
+    for i in rng.choice(count, 200, replace=False):
+        m = data[int(offsets[i]):int(offsets[i] + lengths[i])].tobytes()
+        assert host[i].tobytes() == oracle.hash_one(5, m, 264)
