@@ -175,6 +175,16 @@ class SlotPipeline {
 // bounce buffers (cached per calling thread) and the copy engines take it from there; digests
 // come back the same way.  Pinned callers (b200sha3_pinned_alloc, cudaHostRegister) skip all this.
 
+// Experiment / test knobs: B200SHA3_NO_BOUNCE=1 leaves pageable memory to the driver;
+// B200SHA3_BOUNCE_MIN_KIB and B200SHA3_BOUNCE_BLOCK_KIB shrink the threshold and the block so
+// that small randomized batches (tools/fuzz_parity.py) wrap the ring many times.
+uint64_t env_kib(const char* name, uint64_t fallback_bytes) {
+  const char* env = std::getenv(name);
+  if (!env) return fallback_bytes;
+  const long long kib = std::atoll(env);
+  return kib < 0 ? fallback_bytes : static_cast<uint64_t>(kib) << 10;
+}
+
 bool is_pageable(const void* p) {
   cudaPointerAttributes attr{};
   if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
@@ -187,7 +197,7 @@ bool is_pageable(const void* p) {
 // Helper threads that live for one call; copy() is a parallel memcpy that returns when done.
 class CopyPool {
  public:
-  explicit CopyPool(unsigned helpers) {
+  CopyPool(unsigned helpers, size_t min_parallel_bytes) : min_parallel_(min_parallel_bytes) {
     for (unsigned i = 0; i < helpers; ++i) threads_.emplace_back([this, i] { worker(i + 1); });
   }
   CopyPool(const CopyPool&) = delete;
@@ -203,7 +213,7 @@ class CopyPool {
   }
 
   void copy(void* dst, const void* src, size_t bytes) {
-    if (threads_.empty() || bytes < (1u << 20)) {
+    if (threads_.empty() || bytes < min_parallel_) {
       std::memcpy(dst, src, bytes);
       return;
     }
@@ -242,6 +252,7 @@ class CopyPool {
     }
   }
 
+  const size_t min_parallel_;
   std::vector<std::thread> threads_;
   std::mutex m_;
   std::condition_variable wake_, done_;
@@ -257,7 +268,6 @@ class CopyPool {
 // for a digest block, once it has been copied out to the caller's buffer.
 class BounceRing {
  public:
-  static constexpr size_t kBlock = 8u << 20;
   static constexpr int kSlots = 8;
 
   ~BounceRing() {
@@ -269,6 +279,8 @@ class BounceRing {
 
   cudaError_t init() {
     if (base_) return cudaSuccess;
+    static const size_t block = std::max<uint64_t>(512, env_kib("B200SHA3_BOUNCE_BLOCK_KIB", 8u << 20));
+    kBlock = block;
     cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&base_), kBlock * kSlots, cudaHostAllocPortable);
     for (int i = 0; e == cudaSuccess && i < kSlots; ++i) {
       e = cudaEventCreateWithFlags(&events_[i], cudaEventDisableTiming);
@@ -320,6 +332,8 @@ class BounceRing {
     return first;
   }
 
+  size_t block_bytes() const { return kBlock; }
+
   // After a failed call: forget what was in flight (the streams have been synchronised).
   void abandon() {
     for (int i = 0; i < kSlots; ++i) {
@@ -344,6 +358,7 @@ class BounceRing {
     return release(*slot, pool);
   }
 
+  size_t kBlock = 8u << 20;  // bytes per slot
   uint8_t* base_ = nullptr;
   cudaEvent_t events_[kSlots] = {};
   bool busy_[kSlots] = {};
@@ -361,14 +376,13 @@ thread_local BounceCache t_bounce;
 // bounce ring for pageable memory that is large enough to matter.
 class HostIo {
  public:
-  static constexpr uint64_t kBounceMinBytes = 4u << 20;
-
   // `*_bytes`: what the call will move in total per buffer (decides whether staging pays).
   // `meta` is the offset / length tables of the variable-length entry (one allocation or two:
   // the first one's kind is taken for both).
   cudaError_t init(const void* in, uint64_t in_bytes, const void* out, uint64_t out_bytes,
                    const void* meta = nullptr, uint64_t meta_bytes = 0) {
     static const bool disabled = std::getenv("B200SHA3_NO_BOUNCE") != nullptr;
+    static const uint64_t kBounceMinBytes = std::max<uint64_t>(1, env_kib("B200SHA3_BOUNCE_MIN_KIB", 4u << 20));
     bounce_in_ = !disabled && in && in_bytes >= kBounceMinBytes && is_pageable(in);
     bounce_out_ = !disabled && out && out_bytes >= kBounceMinBytes && is_pageable(out);
     bounce_meta_ = !disabled && meta && meta_bytes >= kBounceMinBytes && is_pageable(meta);
@@ -388,7 +402,8 @@ class HostIo {
       return cudaSuccess;
     }
     const unsigned hw = std::thread::hardware_concurrency();  // helpers + the caller: half the cores, <= 8
-    pool_ = std::make_unique<CopyPool>(hw >= 4 ? std::min(7u, hw / 2 - 1) : 0u);
+    pool_ = std::make_unique<CopyPool>(hw >= 4 ? std::min(7u, hw / 2 - 1) : 0u,
+                                       std::min<size_t>(1u << 20, ring_->block_bytes()));
     return cudaSuccess;
   }
 
