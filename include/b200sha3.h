@@ -141,6 +141,10 @@ B200SHA3_API const char* b200sha3_version(void);
 /* Number of CUDA devices visible to the process (0 if CUDA is unusable). */
 B200SHA3_API int b200sha3_device_count(void);
 
+/* The calling thread's current CUDA device (what `device = -1` resolves to), -1 if CUDA is
+ * unusable.  Lets a host layer hand the caller's device to helper threads it starts. */
+B200SHA3_API int b200sha3_current_device(void);
+
 /* ---- host-buffer entries (the hash_batch drop-in) ------------------------
  * All pointers are HOST pointers.  The call copies the batch to the device
  * (chunked and overlapped with compute when the host memory is pinned), hashes

@@ -226,6 +226,15 @@ const char* b200sha3_last_cuda_error(void) { return last_error_buffer(); }
 
 const char* b200sha3_version(void) { return "b200sha3 0.1 (sm_100a)"; }
 
+int b200sha3_current_device(void) {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return dev;
+}
+
 int b200sha3_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {

@@ -516,6 +516,8 @@ int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_t msg_len, ui
   const uint64_t unit = std::max<uint64_t>(1, msg_len + digest_bytes);
   uint64_t chunk = pipelined ? chunk_target_bytes(unit) / unit : count;
   chunk = std::min(std::max<uint64_t>(chunk, 16), count);
+  const uint64_t nchunks = (count + chunk - 1) / chunk;
+  chunk = (count + nchunks - 1) / nchunks;  // equal chunks: no straggler of a few messages
   SlotPipeline pipe(chunk < count ? kPipelineSlots : 1, c.device_ms != nullptr);
   CU(pipe.init());
   HostIo io;

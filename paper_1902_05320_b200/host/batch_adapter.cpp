@@ -206,8 +206,16 @@ class BatchPipeline {
     t_data_staging.trim(failed_ ? 0 : kKeepBytes);
     t_digest_staging.trim(failed_ ? 0 : kKeepBytes);
     if (error_) std::rethrow_exception(error_);  // first failure wins (batch.cpp:111-130)
+    // Device time of the hashing kernels: lanes of one device are added up (their kernels share
+    // that GPU), devices run side by side.
     double ms = 0.0;
-    for (double d : device_ms_) ms = std::max(ms, d);
+    for (std::size_t a = 0; a < device_ms_.size(); ++a) {
+      double on_device = 0.0;
+      for (std::size_t b = 0; b < device_ms_.size(); ++b) {
+        if (lanes_[b] == lanes_[a]) on_device += device_ms_[b];
+      }
+      ms = std::max(ms, on_device);
+    }
     result_.elapsed = std::chrono::duration<double>(ms * 1e-3);
     if (StageTimes* st = device_.stages) {
       st->scan = scan_s;
@@ -242,6 +250,7 @@ class BatchPipeline {
   static constexpr std::uint64_t kMaxChunkBytes = (1ull << 30) >> kScale;   // ... up to this
   static constexpr std::uint64_t kPoolMinBytes = (4ull << 20) >> kScale;  // below: the caller works alone
   static constexpr std::size_t kParallelScanMin = (1u << 18) >> kScale;   // messages
+  static constexpr int kLanesPerDevice = 2;                               // host threads issuing device calls
   static constexpr std::size_t kRingChunks = 12;                          // pinned staging: chunks in flight
   static constexpr std::uint64_t kRingBytes = (1ull << 30) >> kScale;     // ... and their bytes, at most
   static constexpr std::size_t kResizeStep = (1u << 17) >> kScale;        // digest slots per published step
@@ -294,6 +303,19 @@ class BatchPipeline {
     const std::uint64_t block_bytes = std::max<std::uint64_t>(1, total / nblocks_);
     task_blocks_ = std::max<std::size_t>(1, std::min<std::uint64_t>(kTaskBytes / block_bytes, nblocks_));
     ntasks_ = (nblocks_ + task_blocks_ - 1) / task_blocks_;
+    // Device lanes: two host threads per device issue its C-ABI calls (chunk k -> lane k mod
+    // lanes), so the H2D copy of one chunk overlaps the kernels / D2H of the previous one, and
+    // the kernels of two chunks of few long messages share the GPU.
+    lanes_.clear();
+    static const int lanes_per_device = [] {  // B200SHA3_ADAPTER_LANES: experiment knob
+      const char* env = std::getenv("B200SHA3_ADAPTER_LANES");
+      const int n = env ? std::atoi(env) : 0;
+      return n >= 1 && n <= 8 ? n : kLanesPerDevice;
+    }();
+    for (int rep = 0; rep < lanes_per_device; ++rep) {
+      if (device_.devices.empty()) lanes_.push_back(device_.device);
+      for (int d : device_.devices) lanes_.push_back(d);
+    }
     const std::size_t ndev = std::max<std::size_t>(1, device_.devices.size());
     // A chunk is one kernel launch with one thread per message: long messages get larger
     // chunks so that a launch still carries ~2^15 of them.
@@ -303,7 +325,11 @@ class BatchPipeline {
     want = std::min(ntasks_, std::max(want, ndev));
     chunk_tasks_ = (ntasks_ + want - 1) / want;
     nchunks_ = (ntasks_ + chunk_tasks_ - 1) / chunk_tasks_;
-    devices_used_ = static_cast<unsigned>(std::min(ndev, nchunks_));
+    devices_used_ = static_cast<unsigned>(std::min(lanes_.size(), nchunks_));
+    if (devices_used_ > 1 && lanes_[0] < 0) {  // "current device" is the CALLER's: name it for the lane threads
+      const int current = b200sha3_current_device();
+      for (int& d : lanes_) d = current;
+    }
     threads_ = total < kPoolMinBytes ? 1u : static_cast<unsigned>(std::min<std::size_t>(workers_, ntasks_));
     threads_ = std::max(threads_, devices_used_);
 
@@ -393,7 +419,7 @@ class BatchPipeline {
     const std::size_t first = chunk_first(chunk), n = chunk_first(chunk + 1) - first;
     double ms = 0.0;
     b200sha3_config cfg = make_config(device_, &ms);
-    if (!device_.devices.empty()) cfg.device = device_.devices[slot];
+    cfg.device = lanes_[slot];
     if (device_.devices.size() > 1) cfg.stream = nullptr;
     std::uint8_t* out = chunk_out(chunk);
     const int rc =
@@ -403,7 +429,7 @@ class BatchPipeline {
     if (rc == B200SHA3_ERR_INVALID_ARGUMENT) raise(rc);
     if (rc != B200SHA3_OK) {
       std::string where;
-      if (device_.devices.size() > 1) where = " on device " + std::to_string(device_.devices[slot]);
+      if (device_.devices.size() > 1) where = " on device " + std::to_string(lanes_[slot]);
       throw DeviceError(rc, std::string("b200sha3: ") + b200sha3_strerror(rc) + where + ": " +
                                 b200sha3_last_cuda_error());  // thread-local text: read it here
     }
@@ -533,7 +559,8 @@ class BatchPipeline {
   std::unique_ptr<std::uint64_t[]> block_base_, offsets_, lengths_;
   std::uint64_t first_len_ = 0, total_in_ = 0;
   bool fixed_ = true, speculative_ = false;
-  unsigned threads_ = 1, devices_used_ = 1;
+  unsigned threads_ = 1, devices_used_ = 1;  // devices_used_: device lanes in use
+  std::vector<int> lanes_;                   // CUDA ordinal per lane
   std::size_t ring_ = 1;
   std::uint64_t chunk_in_cap_ = 0, chunk_out_cap_ = 0;
   std::uint8_t* data_ = nullptr;    // ring_ x chunk_in_cap_ bytes, pinned

@@ -41,6 +41,7 @@ uint32_t b200sha3_rate_bytes(int algorithm) {
 const char* b200sha3_strerror(int status) { return status == B200SHA3_OK ? "ok" : "fake device error"; }
 const char* b200sha3_last_cuda_error(void) { return "injected"; }
 int b200sha3_device_count(void) { return 1; }
+int b200sha3_current_device(void) { return 0; }
 
 int b200sha3_pinned_alloc(uint64_t bytes, void** out) {
   *out = std::malloc(bytes ? bytes : 1);  // fresh, unaligned-to-page memory: ASan sees overruns
