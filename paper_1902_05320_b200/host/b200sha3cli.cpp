@@ -126,8 +126,9 @@ int cmd_bench(sha3::Algorithm algorithm, std::uint64_t bits, std::size_t message
     double aggregate = 0;
     while (samples.size() < repeats || aggregate < 1e-3) {
       const auto t0 = std::chrono::steady_clock::now();
-      samples.push_back(sha3::b200::hash_batch(batch, config).elapsed.count());
+      const sha3::BatchResult result = sha3::b200::hash_batch(batch, config);
       walls.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+      samples.push_back(result.elapsed.count());  // `result` dies after the clock was read
       aggregate += samples.back();
       if (samples.size() >= 1u << 20) break;
     }

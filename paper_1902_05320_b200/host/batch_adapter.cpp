@@ -108,7 +108,8 @@ thread_local StagingBuffer t_data_staging, t_digest_staging;
 void advise_huge_pages(void* p, std::size_t bytes) {
 #if defined(__linux__) && defined(MADV_HUGEPAGE)
   constexpr std::uintptr_t kHuge = std::uintptr_t{2} << 20;
-  if (bytes < 2 * kHuge) return;
+  static const bool off = std::getenv("B200SHA3_ADAPTER_NO_THP") != nullptr;  // experiment knob
+  if (bytes < 2 * kHuge || off) return;
   const std::uintptr_t lo = (reinterpret_cast<std::uintptr_t>(p) + kHuge - 1) & ~(kHuge - 1);
   const std::uintptr_t hi = (reinterpret_cast<std::uintptr_t>(p) + bytes) & ~(kHuge - 1);
   if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
@@ -246,10 +247,13 @@ class BatchPipeline {
   static constexpr int kScale = B200SHA3_ADAPTER_TEST_SCALE;
   static constexpr std::uint64_t kTaskBytes = (1ull << 20) >> kScale;     // input + output per task
   static constexpr std::uint64_t kChunkBytes = (32ull << 20) >> kScale;   // input + output per device call ...
+  static constexpr std::uint64_t kMinChunkBytes = (2ull << 20) >> kScale; // ... at least this ...
+  static constexpr std::uint64_t kMinChunks = 8;                          // ... aiming at this many chunks
   static constexpr std::uint64_t kChunkMinMessages = (1u << 15) >> kScale;  // ... grown to hold this many messages
   static constexpr std::uint64_t kMaxChunkBytes = (1ull << 30) >> kScale;   // ... up to this
   static constexpr std::uint64_t kPoolMinBytes = (4ull << 20) >> kScale;  // below: the caller works alone
   static constexpr std::size_t kParallelScanMin = (1u << 18) >> kScale;   // messages
+  static constexpr std::size_t kArenaGrowBytes = 120u << 10;              // < glibc's 128 KiB trim threshold
   static constexpr int kLanesPerDevice = 2;                               // host threads issuing device calls
   static constexpr std::size_t kRingChunks = 12;                          // pinned staging: chunks in flight
   static constexpr std::uint64_t kRingBytes = (1ull << 30) >> kScale;     // ... and their bytes, at most
@@ -319,8 +323,15 @@ class BatchPipeline {
     const std::size_t ndev = std::max<std::size_t>(1, device_.devices.size());
     // A chunk is one kernel launch with one thread per message: long messages get larger
     // chunks so that a launch still carries ~2^15 of them.
+    static const std::uint64_t min_chunks = [] {  // B200SHA3_ADAPTER_MIN_CHUNKS: experiment knob
+      const char* env = std::getenv("B200SHA3_ADAPTER_MIN_CHUNKS");
+      const long n = env ? std::atol(env) : 0;
+      return static_cast<std::uint64_t>(n >= 1 ? n : kMinChunks);
+    }();
+    // ... and mid-size batches get smaller ones, so that there is a pipeline at all
+    const std::uint64_t base_bytes = std::min(kChunkBytes, std::max(kMinChunkBytes, total / min_chunks));
     const std::uint64_t chunk_bytes =
-        std::min(kMaxChunkBytes, std::max(kChunkBytes, total / count_ * kChunkMinMessages));
+        std::min(kMaxChunkBytes, std::max(base_bytes, total / count_ * kChunkMinMessages));
     std::size_t want = static_cast<std::size_t>((total + chunk_bytes / 2) / chunk_bytes);  // nearest
     want = std::min(ntasks_, std::max(want, ndev));
     chunk_tasks_ = (ntasks_ + want - 1) / want;
@@ -411,7 +422,17 @@ class BatchPipeline {
     const std::size_t lo = task_first(task), hi = task_first(task + 1);
     const std::size_t chunk = task / chunk_tasks_;
     const std::uint8_t* d = chunk_out(chunk) + (lo - chunk_first(chunk)) * digest_bytes_;
-    for (std::size_t i = lo; i < hi; ++i, d += digest_bytes_) slots_[i].assign(d, d + digest_bytes_);
+    // One heap allocation per digest is the result type's price.  glibc grows a thread's arena
+    // one page (~85 digests) per mprotect(), and mprotect() takes the process's mmap lock for
+    // writing -- with 16 threads unpacking, that lock is what they queue on.  Allocating and
+    // freeing a block just under the trim threshold first makes the arena grow by that much in
+    // one step; the small allocations that follow are carved from it.  (Any other allocator
+    // just sees a malloc/free pair.)
+    const std::size_t per_grow = std::max<std::size_t>(1, kArenaGrowBytes / (digest_bytes_ + 32));
+    for (std::size_t i = lo; i < hi; ++i, d += digest_bytes_) {
+      if ((i - lo) % per_grow == 0 && digest_bytes_ < kArenaGrowBytes / 4) std::free(std::malloc(kArenaGrowBytes));
+      slots_[i].assign(d, d + digest_bytes_);
+    }
   }
 
   // One C-ABI call for the messages of chunk `chunk` on device slot `slot`.

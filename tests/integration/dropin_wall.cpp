@@ -6,6 +6,7 @@
 // section 9 (row f-3); the reference side is loaded with dlopen and is optional.
 //
 //   dropin_wall [log2_count=20] [message_bytes=64 | 0 = ragged 0..300] [repeats=5]
+//               [reference library | none] [workers=0 (all host threads)]
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -77,13 +78,15 @@ int main(int argc, char** argv) {
   sha3::b200::StageTimes st;
   sha3::b200::DeviceConfig dev;
   dev.stages = &st;
-  sha3::BatchResult ours = sha3::b200::hash_batch(batch, {}, dev);  // warm-up (context, pinning)
+  sha3::EngineConfig engine;
+  engine.workers = argc > 5 ? static_cast<unsigned>(std::atoi(argv[5])) : 0;
+  sha3::BatchResult ours = sha3::b200::hash_batch(batch, engine, dev);  // warm-up (context, pinning)
   std::vector<double> wall, scan, pipe, resize, call, pack, unpack, kern;
   sha3::BatchResult prev;
   for (int r = 0; r < repeats; ++r) {
     prev = std::move(ours);  // keep the old digests alive: their destruction is not part of the call
     const double t0 = now_s();
-    ours = sha3::b200::hash_batch(batch, {}, dev);
+    ours = sha3::b200::hash_batch(batch, engine, dev);
     wall.push_back(now_s() - t0);
     prev = {};
     scan.push_back(st.scan);
