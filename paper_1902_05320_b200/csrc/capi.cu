@@ -142,7 +142,7 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
   const bool bucketing = (c.flags & B200SHA3_FLAG_NO_BUCKETING) == 0;
   for (uint64_t first = 0; first < count; first += kSlice) {
     const uint32_t n = static_cast<uint32_t>(std::min<uint64_t>(kSlice, count - first));
-    uint32_t* scratch = nullptr;  // [0] unaligned flag, then bucket scratch, then order
+    uint32_t* scratch = nullptr;  // [0] unaligned flag, [1] ragged flag, then bucket scratch, then order
     const size_t words = 8 + kBucketScratchWords + (bucketing ? static_cast<size_t>(n) : 0);
     CU(cudaMallocAsync(&scratch, words * sizeof(uint32_t), stream));
     uint32_t* flag = scratch;
@@ -154,7 +154,7 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
                              bucket_scratch, flag, stream));
       if (launches) *launches += 3;
     } else {
-      CU(launch_alignment_check(d_offsets + first, n, flag, stream));
+      CU(launch_alignment_check(d_offsets + first, d_lengths + first, n, 8u * v.rate_lanes, flag, stream));
       if (launches) *launches += 1;
     }
     HashArgs args{};
@@ -164,6 +164,7 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     args.count = n;
     args.order = order;
     args.unaligned_flag = is_aligned(d_data, 8) ? flag : nullptr;
+    args.ragged_flag = flag + 1;
     args.aligned8 = 0u;  // used only when the base pointer itself is misaligned
     args.digests = d_digests + first * digest_bytes;
     args.digest_bytes = digest_bytes;

@@ -67,17 +67,23 @@ bucket_histogram_kernel(const uint64_t* __restrict__ offsets,
   for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) local[i] = 0u;
   __syncthreads();
   const uint32_t base = blockIdx.x * (kBucketThreads * kBucketItems);
-  uint32_t misaligned = 0u;
+  const uint32_t first_tail = static_cast<uint32_t>(lengths[0] % rate_bytes);
+  uint32_t misaligned = 0u, ragged = 0u;
 #pragma unroll
   for (int k = 0; k < kBucketItems; ++k) {
     const uint32_t i = base + k * kBucketThreads + threadIdx.x;
     if (i < count) {
-      atomicAdd(&local[bucket_key(lengths[i], rate_bytes)], 1u);
+      const uint64_t len = lengths[i];
+      atomicAdd(&local[bucket_key(len, rate_bytes)], 1u);
       misaligned |= static_cast<uint32_t>(offsets[i]) & 7u;
+      ragged |= static_cast<uint32_t>(len % rate_bytes) ^ first_tail;
     }
   }
   if (__any_sync(0xffffffffu, misaligned != 0u) && (threadIdx.x & 31) == 0) {
     atomicOr(unaligned_flag, 1u);
+  }
+  if (__any_sync(0xffffffffu, ragged != 0u) && (threadIdx.x & 31) == 0) {
+    atomicOr(unaligned_flag + 1, 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) {
@@ -134,15 +140,20 @@ bucket_scatter_kernel(const uint64_t* __restrict__ lengths, uint32_t count,
 }
 
 __global__ void __launch_bounds__(256)
-alignment_check_kernel(const uint64_t* __restrict__ offsets, uint64_t count,
-                       uint32_t* __restrict__ unaligned_flag) {
-  uint32_t misaligned = 0u;
+alignment_check_kernel(const uint64_t* __restrict__ offsets, const uint64_t* __restrict__ lengths,
+                       uint64_t count, uint32_t rate_bytes, uint32_t* __restrict__ unaligned_flag) {
+  const uint32_t first_tail = static_cast<uint32_t>(lengths[0] % rate_bytes);
+  uint32_t misaligned = 0u, ragged = 0u;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     misaligned |= static_cast<uint32_t>(offsets[i]) & 7u;
+    ragged |= static_cast<uint32_t>(lengths[i] % rate_bytes) ^ first_tail;
   }
   if (__any_sync(0xffffffffu, misaligned != 0u) && (threadIdx.x & 31) == 0) {
     atomicOr(unaligned_flag, 1u);
+  }
+  if (__any_sync(0xffffffffu, ragged != 0u) && (threadIdx.x & 31) == 0) {
+    atomicOr(unaligned_flag + 1, 1u);
   }
 }
 
@@ -247,10 +258,10 @@ cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths
   return cudaGetLastError();
 }
 
-cudaError_t launch_alignment_check(const uint64_t* offsets, uint64_t count,
-                                   uint32_t* unaligned_flag, cudaStream_t stream) {
+cudaError_t launch_alignment_check(const uint64_t* offsets, const uint64_t* lengths, uint64_t count,
+                                   uint32_t rate_bytes, uint32_t* unaligned_flag, cudaStream_t stream) {
   if (count == 0) return cudaSuccess;
-  alignment_check_kernel<<<grid_for(count, 256), 256, 0, stream>>>(offsets, count,
+  alignment_check_kernel<<<grid_for(count, 256), 256, 0, stream>>>(offsets, lengths, count, rate_bytes,
                                                                   unaligned_flag);
   return cudaGetLastError();
 }

@@ -24,9 +24,10 @@ hash_generic_kernel(const HashArgs args) {
   const uint64_t len = args.lengths ? args.lengths[m] : args.fixed_len;
   const bool aligned8 =
       args.unaligned_flag ? (*args.unaligned_flag == 0u) : (args.aligned8 != 0u);
+  const bool ragged = args.ragged_flag != nullptr && *args.ragged_flag != 0u;
   hash_message<RL, UNROLL, FMA_MASK>(args.data + off, len,
                                      args.digests + m * args.digest_bytes,
-                                     args.digest_bytes, args.head, args.last_mask, aligned8);
+                                     args.digest_bytes, args.head, args.last_mask, aligned8, ragged);
 }
 
 template <int RL, int UNROLL, int PRESET>

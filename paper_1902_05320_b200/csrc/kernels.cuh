@@ -17,6 +17,8 @@ struct HashArgs {
   const uint32_t* order;     // processing order (bucketed), or nullptr: identity
   const uint32_t* unaligned_flag;  // device word, nonzero if any message start is not
                                    // 8-byte aligned; nullptr: use `aligned8`
+  const uint32_t* ragged_flag;     // device word, nonzero if the final (partial) blocks of the
+                                   // batch differ in length; nullptr: they are all alike
   uint8_t* digests;          // count * digest_bytes, message order
   uint64_t digest_bytes;
   uint32_t head;             // pad head byte: 0x06 / 0x1f
@@ -74,18 +76,19 @@ cudaError_t launch_hash_staged(const HashArgs& args, const LaunchPlan& plan, cud
 // Keccak-f[1600] on raw 200-byte states (test hook).
 cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream);
 
-// Bucketing by block count: writes a processing order (heaviest first) and sets
-// *unaligned_flag if any offset is not a multiple of 8.  `scratch` needs
-// kBucketScratchWords 32-bit words.
+// Bucketing by block count: writes a processing order (heaviest first), sets
+// *unaligned_flag if any offset is not a multiple of 8 and unaligned_flag[1] (the "ragged"
+// word) if the messages do not all leave the same number of bytes for the final block.
+// `scratch` needs kBucketScratchWords 32-bit words.
 constexpr int kBucketBins = 256;
 constexpr int kBucketScratchWords = 2 * kBucketBins + 8;
 cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,
                                 uint32_t count, uint32_t rate_bytes, uint32_t* order,
                                 uint32_t* scratch, uint32_t* unaligned_flag,
                                 cudaStream_t stream);
-// Alignment check only (no ordering).
-cudaError_t launch_alignment_check(const uint64_t* offsets, uint64_t count,
-                                   uint32_t* unaligned_flag, cudaStream_t stream);
+// The two flag words only (no ordering).
+cudaError_t launch_alignment_check(const uint64_t* offsets, const uint64_t* lengths, uint64_t count,
+                                   uint32_t rate_bytes, uint32_t* unaligned_flag, cudaStream_t stream);
 
 // Synthetic workloads.
 cudaError_t launch_generate_workload(uint64_t stream_seed, uint64_t message_size,

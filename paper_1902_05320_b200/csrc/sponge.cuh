@@ -65,10 +65,37 @@ __device__ __forceinline__ void absorb_words_unaligned(State& a, const uint8_t* 
 // Final (partial) block: `rem` < 8*RL message bytes at p, then the pad.
 //   head = suffix | 1 << suffix_bits  (0x06 / 0x1f), XORed at byte `rem`;
 //   0x80 XORed at byte 8*RL - 1 (the same byte when rem == 8*RL - 1).
+//
+// `ragged`: the threads of a warp hold final blocks of different lengths.  The jump table
+// below would then run its cases one after the other (up to RL + 1 of them, each waiting
+// for its own loads); the ragged form is the same work as RL predicated 8-byte loads, two
+// 4-byte loads for the partial lane (nothing is read outside the aligned 4-byte words that
+// hold message bytes) and predicated XORs -- ~6 ALU instructions per lane, no divergence.
 template <int RL>
 __device__ __forceinline__ void absorb_tail(State& a, const uint8_t* p, uint32_t rem,
-                                            uint32_t head, bool aligned8) {
-  if (aligned8) {
+                                            uint32_t head, bool aligned8, bool ragged = false) {
+  if (aligned8 && ragged) {
+    const uint32_t fl = rem >> 3, rb = rem & 7u;
+    const uint2* q = reinterpret_cast<const uint2*>(p);
+    const uint32_t* tq = reinterpret_cast<const uint32_t*>(p + 8u * fl);
+    uint32_t tlo = rb != 0u ? ld_u32(tq) : 0u;
+    uint32_t thi = rb > 4u ? ld_u32(tq + 1) : 0u;
+    tlo &= rb >= 4u ? 0xffffffffu : (1u << (8u * rb)) - 1u;
+    thi &= rb > 4u ? (1u << (8u * (rb - 4u))) - 1u : 0u;
+    if (rb < 4u) {
+      tlo |= head << (8u * rb);
+    } else {
+      thi |= head << (8u * (rb - 4u));
+    }
+#pragma unroll
+    for (int i = 0; i < RL; ++i) {
+      uint2 v = make_uint2(0u, 0u);
+      if (static_cast<uint32_t>(i) < fl) v = ld_u2(q + i);
+      if (static_cast<uint32_t>(i) == fl) v = make_uint2(tlo, thi);
+      a.lo[i] ^= v.x;
+      a.hi[i] ^= v.y;
+    }
+  } else if (aligned8) {
     const uint32_t fl = rem >> 3, rb = rem & 7u;
     const uint8_t* tp = p + 8u * fl;
     uint32_t tlo = 0u, thi = 0u;
@@ -220,7 +247,7 @@ __device__ __forceinline__ void emit_block(const State& a, uint8_t* o, uint32_t 
 template <int RL, int UNROLL, uint32_t FMA_MASK>
 __device__ __forceinline__ void hash_message(const uint8_t* p, uint64_t len, uint8_t* out,
                                              uint64_t out_len, uint32_t head,
-                                             uint32_t last_mask, bool aligned8) {
+                                             uint32_t last_mask, bool aligned8, bool ragged = false) {
   constexpr uint32_t R = 8u * RL;
   State a;
   state_zero(a);
@@ -240,7 +267,7 @@ __device__ __forceinline__ void hash_message(const uint8_t* p, uint64_t len, uin
       left_in -= R;
     }
   }
-  absorb_tail<RL>(a, p, static_cast<uint32_t>(left_in), head, aligned8);
+  absorb_tail<RL>(a, p, static_cast<uint32_t>(left_in), head, aligned8, ragged);
   keccak_f1600<UNROLL, FMA_MASK>(a);
   uint8_t* o = out;
   uint64_t left = out_len;
