@@ -15,15 +15,16 @@ from paper_1902_05320_b200.engine import FLAG_NO_BUCKETING  # noqa: E402
 probe = Engine(device=0)
 peak, _ = probe.probe_pipe(2)
 out = []
+pack = int(sys.argv[1]) if len(sys.argv) > 1 else 8      # message starts are multiples of this
 for log2_count, max_len in [(22, 300), (22, 1000), (20, 300), (24, 135), (22, 4096)]:
     count = 1 << log2_count
     g = torch.Generator(device="cuda").manual_seed(3)
     lengths = torch.randint(0, max_len + 1, (count,), generator=g, device="cuda", dtype=torch.int64)
-    padded = (lengths + 7) // 8 * 8
+    padded = (lengths + pack - 1) // pack * pack
     offsets = torch.cumsum(padded, 0) - padded
     data = torch.randint(0, 256, (int(padded.sum().item()) + 16,), dtype=torch.uint8, device="cuda")
     perms = int((lengths // 136 + 1).sum().item())
-    rec = {"messages": count, "max_len": max_len, "permutations": perms}
+    rec = {"messages": count, "max_len": max_len, "start_alignment": pack, "permutations": perms}
     for name, flags in (("bucketed", 0), ("input_order", FLAG_NO_BUCKETING)):
         eng = Engine(device=0, flags=flags)
         best = None
@@ -35,4 +36,4 @@ for log2_count, max_len in [(22, 300), (22, 1000), (20, 300), (24, 135), (22, 40
     out.append(rec)
     print(json.dumps(rec), flush=True)
 (ROOT / "gpurun_out").mkdir(exist_ok=True)
-(ROOT / "gpurun_out" / "short_ragged.json").write_text(json.dumps(out, indent=1))
+(ROOT / "gpurun_out" / f"short_ragged_align{pack}.json").write_text(json.dumps(out, indent=1))
