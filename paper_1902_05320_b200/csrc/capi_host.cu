@@ -111,7 +111,8 @@ class SlotPipeline {
   template <class T>
   cudaError_t alloc(int s, T** out, uint64_t bytes) {
     void* p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, std::max<uint64_t>(bytes, 16), streams_[s]);
+    // whole 16-byte units: the kernels read the aligned 4-byte words that hold message bytes
+    cudaError_t e = cudaMallocAsync(&p, (std::max<uint64_t>(bytes, 16) + 15) & ~uint64_t{15}, streams_[s]);
     if (e == cudaSuccess) buffers_[s].push_back(p);
     *out = static_cast<T*>(p);
     return e;
