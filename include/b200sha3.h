@@ -255,6 +255,20 @@ B200SHA3_API int b200sha3_states_finish_device(b200sha3_states* states, uint64_t
 B200SHA3_API int b200sha3_states_squeeze_device(b200sha3_states* states, uint64_t out_bytes,
                                                 uint8_t* d_out, const b200sha3_config* cfg);
 
+/* The same four steps on HOST buffers (what a caller of sha3::Hasher holds): the chunk bytes are
+ * staged to the device (pinned memory: straight DMA; pageable memory: through the library's
+ * bounce ring), the device form runs on cfg->stream, and the call returns when the host
+ * buffers are free again (update) or filled (finish / squeeze). */
+B200SHA3_API int b200sha3_states_update(b200sha3_states* states, const uint8_t* data,
+                                        const uint64_t* offsets, const uint64_t* lengths,
+                                        const b200sha3_config* cfg);
+B200SHA3_API int b200sha3_states_update_fixed(b200sha3_states* states, const uint8_t* data,
+                                              uint64_t chunk_len, const b200sha3_config* cfg);
+B200SHA3_API int b200sha3_states_finish(b200sha3_states* states, uint64_t xof_output_bits,
+                                        uint8_t* digests, const b200sha3_config* cfg);
+B200SHA3_API int b200sha3_states_squeeze(b200sha3_states* states, uint64_t out_bytes, uint8_t* out,
+                                         const b200sha3_config* cfg);
+
 /* ---- pipe microbenchmark ---------------------------------------------------
  * Measures the issue rate of one instruction mix on the current device:
  * returns thread-instructions per second through *instr_per_s, and the SM

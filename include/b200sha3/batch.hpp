@@ -120,4 +120,43 @@ std::vector<std::uint8_t> hash_packed(Algorithm algorithm, const std::uint8_t* d
                                       const DeviceConfig& device = {},
                                       double* elapsed_seconds = nullptr);
 
+// `count` incremental hashers on the device: the batch form of sha3::Hasher
+// (proj/core/include/sha3/sha3.hpp:66-86, proj/core/src/sha3.cpp:95-130).  update() feeds
+// chunk i to stream i (any chunking gives the one-shot digest, proj/tests/test_sponge.cpp:114-132);
+// digest() finalises the hash variants; finish() + read() stream XOF output
+// (proj/tests/test_sponge.cpp:134-150).  Misuse throws std::logic_error with the reference's
+// messages (sha3.cpp:103-126, sponge.cpp:82-84, :114-116, :132-134).  Single owner; movable.
+class BatchHasher {
+ public:
+  BatchHasher(Algorithm algorithm, std::size_t count, const DeviceConfig& device = {});
+  ~BatchHasher();
+  BatchHasher(BatchHasher&& other) noexcept;
+  BatchHasher& operator=(BatchHasher&& other) noexcept;
+  BatchHasher(const BatchHasher&) = delete;
+  BatchHasher& operator=(const BatchHasher&) = delete;
+
+  // chunks.size() must equal count(); chunks[i] may be empty.
+  void update(const std::vector<std::vector<std::uint8_t>>& chunks);
+  // The same on a packed buffer: chunk i is data[offsets[i], offsets[i] + lengths[i]).
+  void update(const std::uint8_t* data, const std::uint64_t* offsets, const std::uint64_t* lengths);
+  // Equal-length chunks back to back: chunk i is data[i * chunk_len, (i + 1) * chunk_len).
+  void update_fixed(const std::uint8_t* data, std::uint64_t chunk_len);
+
+  std::vector<std::vector<std::uint8_t>> digest();                   // hash variants only
+  void finish();                                                     // XOF variants only
+  std::vector<std::vector<std::uint8_t>> read(std::size_t nbytes);   // XOF, after finish()
+
+  Algorithm algorithm() const { return algorithm_; }
+  std::size_t count() const { return count_; }
+  void reset();
+
+ private:
+  void check(int status) const;
+  std::vector<std::vector<std::uint8_t>> split(const std::vector<std::uint8_t>& packed, std::size_t each) const;
+  Algorithm algorithm_;
+  std::size_t count_;
+  DeviceConfig device_;
+  b200sha3_states* states_ = nullptr;
+};
+
 }  // namespace sha3::b200

@@ -616,4 +616,123 @@ BatchResult hash_batch(const HashBatch& batch, const EngineConfig& config,
   return result;
 }
 
+// ---------------------------------------------------------------------------------------
+// BatchHasher: sha3::Hasher for `count` streams at once, over the b200sha3_states_* entries.
+
+BatchHasher::BatchHasher(Algorithm algorithm, std::size_t count, const DeviceConfig& device)
+    : algorithm_(algorithm), count_(count), device_(device) {
+  const int alg = static_cast<int>(algorithm);
+  if (alg < 0 || alg > 5) throw std::invalid_argument("BatchHasher: unknown algorithm");
+  device_.stages = nullptr;
+  b200sha3_config cfg = make_config(device_, nullptr);
+  if (!device_.devices.empty()) cfg.device = device_.devices[0];
+  check(b200sha3_states_create(alg, count, &cfg, &states_));
+}
+
+BatchHasher::~BatchHasher() {
+  if (states_) b200sha3_states_destroy(states_);
+}
+
+BatchHasher::BatchHasher(BatchHasher&& other) noexcept
+    : algorithm_(other.algorithm_), count_(other.count_), device_(std::move(other.device_)),
+      states_(other.states_) {
+  other.states_ = nullptr;
+}
+
+BatchHasher& BatchHasher::operator=(BatchHasher&& other) noexcept {
+  if (this != &other) {
+    if (states_) b200sha3_states_destroy(states_);
+    algorithm_ = other.algorithm_;
+    count_ = other.count_;
+    device_ = std::move(other.device_);
+    states_ = other.states_;
+    other.states_ = nullptr;
+  }
+  return *this;
+}
+
+void BatchHasher::check(int status) const {
+  if (status == B200SHA3_OK) return;
+  if (status == B200SHA3_ERR_STATE) {  // the reference's std::logic_error (sponge.cpp:82-84, :114-116, :132-134)
+    throw std::logic_error("BatchHasher: call out of order (update after finish, finish twice, or read before finish)");
+  }
+  if (status == B200SHA3_ERR_INVALID_ARGUMENT) throw std::invalid_argument("BatchHasher: invalid argument");
+  throw DeviceError(status, std::string("b200sha3: ") + b200sha3_strerror(status) + ": " +
+                                b200sha3_last_cuda_error());
+}
+
+void BatchHasher::update(const std::uint8_t* data, const std::uint64_t* offsets,
+                         const std::uint64_t* lengths) {
+  b200sha3_config cfg = make_config(device_, nullptr);
+  check(b200sha3_states_update(states_, data, offsets, lengths, &cfg));
+}
+
+void BatchHasher::update_fixed(const std::uint8_t* data, std::uint64_t chunk_len) {
+  b200sha3_config cfg = make_config(device_, nullptr);
+  check(b200sha3_states_update_fixed(states_, data, chunk_len, &cfg));
+}
+
+void BatchHasher::update(const std::vector<std::vector<std::uint8_t>>& chunks) {
+  if (chunks.size() != count_) throw std::invalid_argument("BatchHasher: one chunk per stream expected");
+  std::vector<std::uint64_t> offsets(count_), lengths(count_);
+  std::uint64_t total = 0;
+  for (std::size_t i = 0; i < count_; ++i) {
+    offsets[i] = total;
+    lengths[i] = chunks[i].size();
+    total += lengths[i];
+  }
+  std::uint8_t* data = t_data_staging.reserve(std::max<std::uint64_t>(total, 16));
+  parallel_ranges(count_, pack_workers(EngineConfig{}), total, [&](std::size_t begin, std::size_t end) {
+    for (std::size_t i = begin; i < end; ++i) {
+      if (lengths[i]) std::memcpy(data + offsets[i], chunks[i].data(), lengths[i]);
+    }
+  });
+  update(data, offsets.data(), lengths.data());
+  t_data_staging.trim(kKeepBytes);
+}
+
+std::vector<std::vector<std::uint8_t>> BatchHasher::split(const std::vector<std::uint8_t>& packed,
+                                                          std::size_t each) const {
+  std::vector<std::vector<std::uint8_t>> out(count_);
+  for (std::size_t i = 0; i < count_; ++i) {
+    out[i].assign(packed.begin() + i * each, packed.begin() + (i + 1) * each);
+  }
+  return out;
+}
+
+std::vector<std::vector<std::uint8_t>> BatchHasher::digest() {
+  const int alg = static_cast<int>(algorithm_);
+  if (alg >= 4) {  // sha3.cpp:103-106
+    throw std::logic_error("Hasher: digest() is for fixed-output variants; use finish()/read()");
+  }
+  const std::size_t each = b200sha3_digest_bytes(alg, 0);
+  std::vector<std::uint8_t> packed(std::max<std::size_t>(count_ * each, 1));
+  b200sha3_config cfg = make_config(device_, nullptr);
+  check(b200sha3_states_finish(states_, 0, packed.data(), &cfg));
+  return split(packed, each);
+}
+
+void BatchHasher::finish() {
+  if (static_cast<int>(algorithm_) < 4) {  // sha3.cpp:111-114
+    throw std::logic_error("Hasher: finish()/read() is for XOF variants; use digest()");
+  }
+  b200sha3_config cfg = make_config(device_, nullptr);
+  check(b200sha3_states_finish(states_, 0, nullptr, &cfg));
+}
+
+std::vector<std::vector<std::uint8_t>> BatchHasher::read(std::size_t nbytes) {
+  if (static_cast<int>(algorithm_) < 4) {  // sha3.cpp:119-122
+    throw std::logic_error("Hasher: finish()/read() is for XOF variants; use digest()");
+  }
+  std::vector<std::uint8_t> packed(std::max<std::size_t>(count_ * nbytes, 1));
+  b200sha3_config cfg = make_config(device_, nullptr);
+  check(b200sha3_states_squeeze(states_, nbytes, packed.data(), &cfg));
+  return split(packed, nbytes);
+}
+
+void BatchHasher::reset() {
+  b200sha3_config cfg = make_config(device_, nullptr);
+  check(b200sha3_states_reset(states_, &cfg));
+}
+
 }  // namespace sha3::b200

@@ -295,6 +295,101 @@ void gpu_cases() {
     }
     CHECK(threw);
   }
+  {  // BatchHasher: sha3::Hasher for N streams at once on HOST buffers.  Restates
+     // proj/tests/test_sponge.cpp:114-150 (any chunking == one shot; XOF output read in pieces ==
+     // one shot) and proj/tests/test_sha3.cpp:205-246 (digest / finish / read misuse throws
+     // std::logic_error, reset gives fresh states).
+    Rng rng(61);
+    const std::size_t n = 300;
+    for (int a = 0; a < 6; ++a) {
+      const Algorithm alg = static_cast<Algorithm>(a);
+      std::vector<std::vector<std::uint8_t>> whole(n);
+      for (auto& m : whole) m = random_bytes(rng, rng.below(700));
+      whole[0].clear();
+      b200::BatchHasher h(alg, n);
+      CHECK(h.count() == n && h.algorithm() == alg);
+      for (int round = 0; round < 3; ++round) {  // message i arrives in three pieces, some empty
+        std::vector<std::vector<std::uint8_t>> chunks(n);
+        for (std::size_t i = 0; i < n; ++i) {
+          const std::size_t len = whole[i].size();
+          const std::size_t c1 = len ? (i * 7 + 3) % (len + 1) : 0, c2 = c1 + (len - c1) / 2;
+          const std::size_t lo = round == 0 ? 0 : (round == 1 ? c1 : c2);
+          const std::size_t hi = round == 0 ? c1 : (round == 1 ? c2 : len);
+          chunks[i].assign(whole[i].begin() + lo, whole[i].begin() + hi);
+        }
+        h.update(chunks);
+      }
+      bool ok = true;
+      if (a < 4) {
+        const auto got = h.digest();
+        for (std::size_t i = 0; i < n; ++i) ok = ok && got[i] == expect(alg, whole[i]);
+        bool threw = false;
+        try { h.update(whole); } catch (const std::logic_error&) { threw = true; }   // update after digest
+        CHECK(threw);
+        threw = false;
+        try { h.finish(); } catch (const std::logic_error&) { threw = true; }        // finish() on a hash variant
+        CHECK(threw);
+      } else {
+        bool threw = false;
+        try { h.read(8); } catch (const std::logic_error&) { threw = true; }         // read before finish
+        CHECK(threw);
+        threw = false;
+        try { h.digest(); } catch (const std::logic_error&) { threw = true; }        // digest() on an XOF
+        CHECK(threw);
+        h.finish();
+        threw = false;
+        try { h.finish(); } catch (const std::logic_error&) { threw = true; }        // finish twice
+        CHECK(threw);
+        const auto p1 = h.read(5), p2 = h.read(200), p3 = h.read(295);               // 500 bytes in pieces
+        for (std::size_t i = 0; i < n; ++i) {
+          std::vector<std::uint8_t> all = p1[i];
+          all.insert(all.end(), p2[i].begin(), p2[i].end());
+          all.insert(all.end(), p3[i].begin(), p3[i].end());
+          ok = ok && all == expect(alg, whole[i], 4000);
+        }
+      }
+      CHECK(ok);
+      h.reset();                                                                     // Hasher::reset
+      std::vector<std::uint8_t> flat(n * 24);
+      for (auto& b : flat) b = static_cast<std::uint8_t>(rng.next());
+      h.update_fixed(flat.data(), 24);
+      b200::BatchHasher moved = std::move(h);
+      ok = true;
+      if (a < 4) {
+        const auto got = moved.digest();
+        for (std::size_t i = 0; i < n; ++i) {
+          ok = ok && got[i] == expect(alg, std::vector<std::uint8_t>(flat.begin() + 24 * i, flat.begin() + 24 * (i + 1)));
+        }
+      } else {
+        moved.finish();
+        const auto got = moved.read(17);
+        for (std::size_t i = 0; i < n; ++i) {
+          ok = ok && got[i] == expect(alg, std::vector<std::uint8_t>(flat.begin() + 24 * i, flat.begin() + 24 * (i + 1)), 136);
+        }
+      }
+      CHECK(ok);
+    }
+    {  // one long input fed in 1 MiB pieces to 64 streams (each its own 3 MiB message)
+      const std::size_t streams = 64, piece = 1u << 20;
+      std::vector<std::vector<std::uint8_t>> whole(streams);
+      b200::BatchHasher h(Algorithm::sha3_256, streams);
+      for (int k = 0; k < 3; ++k) {
+        std::vector<std::uint8_t> flat(streams * piece);
+        for (std::size_t i = 0; i < flat.size(); i += 8) {
+          const std::uint64_t w = rng.next();
+          std::memcpy(flat.data() + i, &w, 8);
+        }
+        for (std::size_t i = 0; i < streams; ++i) {
+          whole[i].insert(whole[i].end(), flat.begin() + i * piece, flat.begin() + (i + 1) * piece);
+        }
+        h.update_fixed(flat.data(), piece);   // pageable memory, 64 MiB: the bounce ring
+      }
+      const auto got = h.digest();
+      bool ok = true;
+      for (std::size_t i = 0; i < streams; i += 9) ok = ok && got[i] == expect(Algorithm::sha3_256, whole[i]);
+      CHECK(ok);
+    }
+  }
   {  // hash_packed on caller-packed buffers with odd offsets
     const std::vector<std::uint8_t> data = {9, 9, 9, 'a', 'b', 'c', 7, 7, 1, 2, 3, 4, 5};
     const std::uint64_t offsets[] = {3, 8, 0}, lengths[] = {3, 5, 0};
