@@ -291,6 +291,10 @@ def main():
     clocks = sampler.stop() if rank == 0 else None
     seconds = max_over_ranks(start.elapsed_time(stop) * 1e-3)
     launches = engine.total_kernel_launches - launches_before
+    if world > 1:  # every rank's kernels count: sum over ranks
+        n = torch.tensor([launches], dtype=torch.int64, device=reduce_device)
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        launches = int(n.item())
     value = total * args.steps / seconds
 
     # checksum of the digests: sum of their 64-bit words mod 2^64 -- proves the timed
