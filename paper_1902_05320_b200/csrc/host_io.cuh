@@ -26,7 +26,7 @@ namespace b200sha3::capi {
 
 // Experiment / test knobs: B200SHA3_NO_BOUNCE=1 leaves pageable memory to the driver;
 // B200SHA3_BOUNCE_MIN_KIB and B200SHA3_BOUNCE_BLOCK_KIB shrink the threshold and the block so
-// that small randomized batches (tools/fuzz_parity.py) wrap the ring many times.
+// that small randomized batches (tests/fuzz_parity.py) wrap the ring many times.
 inline uint64_t env_kib(const char* name, uint64_t fallback_bytes) {
   const char* env = std::getenv(name);
   if (!env) return fallback_bytes;

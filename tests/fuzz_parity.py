@@ -1,6 +1,7 @@
 #!/usr/bin/env python3
 """Randomized differential run: the CUDA path (every entry point and kernel selection)
-against the CPU oracle, for a wall-clock budget.  usage: fuzz_parity.py SECONDS [SEED]
+against the CPU oracle, for a wall-clock budget.  Test infrastructure (it imports the oracle, which
+only code under tests/ may do); not collected by pytest.  usage: python tests/fuzz_parity.py SECONDS [SEED]
 Writes gpurun_out/fuzz_parity.json; exits 1 on the first mismatch (after dumping the case)."""
 import json
 import pathlib
