@@ -48,6 +48,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true")
     # validation only (one-GPU box): run N ranks on the SAME device with a gloo process group
     # to exercise the multi-rank code path; numbers from such a run are not benchmark values
     ap.add_argument("--share-gpu", action="store_true", help=argparse.SUPPRESS)
@@ -226,6 +227,29 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def dropin_cpp_wall(log2_messages: int = 24):
+    """The same metric one level further out: the reference's own C++ interface,
+    sha3::hash_batch on vector<vector<uint8_t>> (proj/core/include/sha3/batch.hpp:23-65), served by
+    the drop-in adapter -- pack + H2D + kernels + D2H + unpack all inside the call, wall clock.
+    Measured by tests/cpp/dropin_wall (tests/integration/dropin_wall.cpp) in its own process;
+    None if that binary was not built."""
+    exe = ROOT / "tests" / "cpp" / "dropin_wall"
+    if not exe.exists():
+        return None
+    try:
+        out = subprocess.run([str(exe), str(log2_messages), str(MSG_LEN), "5", "none"], capture_output=True,
+                             text=True, timeout=300, cwd=str(ROOT))
+        rec = json.loads(out.stdout)
+        d = rec["b200_dropin"]
+        return {"value": d["hashes_per_s"], "unit": "hashes/s", "messages_per_call": rec["count"],
+                "wall_ms_per_call": d["wall_s"] * 1e3, "host_threads": rec["host_threads"],
+                "stages_ms": {k: d[k] * 1e3 for k in ("resize_s", "device_calls_s", "pack_cpu_s", "unpack_cpu_s")},
+                "note": "sha3::b200::hash_batch(HashBatch) -> BatchResult on vector<vector<uint8_t>>, "
+                        "median of 5 calls; pack/unpack CPU times are summed over the host threads"}
+    except (OSError, ValueError, KeyError, subprocess.SubprocessError):
+        return None
+
+
 # --------------------------------------------------------------------------
 def main():
     args = parse_args()
@@ -399,6 +423,10 @@ def main():
         }
         if e2e:
             line["e2e"] = e2e
+        if world == 1 and not args.no_dropin:
+            dropin = dropin_cpp_wall()
+            if dropin:
+                line["dropin_cpp"] = dropin
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"], _ = cpu_baseline(args.cpu_log2_messages, 5, 1)
         print(json.dumps(line), flush=True)
