@@ -174,31 +174,6 @@ struct HostChunk {
   uint64_t lo, hi;        // byte range of `data` the chunk reads (lo is 16-byte aligned)
 };
 
-// Chunks of a packed batch (offsets non-decreasing, messages not overlapping -- what the
-// C++ adapter and every sane caller produce).  Returns false for any other layout.
-bool plan_ordered_chunks(const uint64_t* offsets, const uint64_t* lengths, uint64_t count,
-                         uint64_t target_bytes, std::vector<HostChunk>* chunks) {
-  uint64_t prev_end = 0;
-  HostChunk cur{0, 0, 0, 0};
-  for (uint64_t i = 0; i < count; ++i) {
-    const uint64_t end = offsets[i] + lengths[i];
-    if (offsets[i] < prev_end || end < offsets[i]) return false;
-    if (cur.count == 0) {
-      cur.first = i;
-      cur.lo = offsets[i] & ~15ull;
-    }
-    cur.count += 1;
-    cur.hi = end;
-    prev_end = end;
-    if (cur.hi - cur.lo >= target_bytes || cur.count >= (1ull << 22)) {
-      chunks->push_back(cur);
-      cur = HostChunk{0, 0, 0, 0};
-    }
-  }
-  if (cur.count) chunks->push_back(cur);
-  return true;
-}
-
 // One chunk holding the whole batch: the byte range [lo, hi) that its messages touch.
 HostChunk whole_batch_chunk(const uint64_t* offsets, const uint64_t* lengths, uint64_t count) {
   uint64_t lo = ~0ull, hi = 0;
@@ -210,6 +185,59 @@ HostChunk whole_batch_chunk(const uint64_t* offsets, const uint64_t* lengths, ui
   if (hi == 0) lo = 0;
   return HostChunk{0, count, lo & ~15ull, hi};  // device copy congruent to the host buffer mod 16
 }
+
+// Chunks of a packed batch, planned one at a time while the previous ones are already in
+// flight (reading 16 bytes of offsets / lengths per message for the whole batch first would
+// cost a 2^24-message call ~30 ms before its first copy).  Messages in order and not
+// overlapping -- what the C++ adapter and every sane caller produce -- are cut at
+// `target_bytes`; from the first message that breaks the order on, the rest of the batch is
+// one chunk (one copy of the byte range it touches).
+class ChunkPlanner {
+ public:
+  ChunkPlanner(const uint64_t* offsets, const uint64_t* lengths, uint64_t count, uint64_t target_bytes,
+               bool pipelined)
+      : offsets_(offsets), lengths_(lengths), count_(count), target_(target_bytes), pipelined_(pipelined) {}
+
+  bool next(HostChunk* out) {
+    if (next_ >= count_) return false;
+    if (!pipelined_) return rest(out);
+    HostChunk cur{next_, 0, 0, 0};
+    for (uint64_t i = next_; i < count_; ++i) {
+      const uint64_t end = offsets_[i] + lengths_[i];
+      if (offsets_[i] < prev_end_ || end < offsets_[i]) {  // out of order (or wrapping)
+        if (cur.count == 0) return rest(out);
+        *out = cur;  // close the chunk in progress; the next call takes the rest
+        next_ = i;
+        return true;
+      }
+      if (cur.count == 0) cur.lo = offsets_[i] & ~15ull;
+      cur.count += 1;
+      cur.hi = end;
+      prev_end_ = end;
+      if (cur.hi - cur.lo >= target_ || cur.count >= (1ull << 22)) {
+        *out = cur;
+        next_ = i + 1;
+        return true;
+      }
+    }
+    *out = cur;
+    next_ = count_;
+    return true;
+  }
+
+ private:
+  bool rest(HostChunk* out) {
+    *out = whole_batch_chunk(offsets_ + next_, lengths_ + next_, count_ - next_);
+    out->first = next_;
+    next_ = count_;
+    return true;
+  }
+  const uint64_t* offsets_;
+  const uint64_t* lengths_;
+  uint64_t count_, target_;
+  bool pipelined_;
+  uint64_t next_ = 0, prev_end_ = 0;
+};
 
 int finish_call(int rc, SlotPipeline& pipe, HostIo& io, const Config& c, uint32_t launches) {
   double kernel_ms = 0.0;
@@ -300,47 +328,48 @@ int b200sha3_hash_batch(int algorithm, const uint8_t* data, const uint64_t* offs
   if (c.kernel_launches) *c.kernel_launches = 0;
   if (count == 0) return B200SHA3_OK;
   if (!digests || !offsets || !lengths) return B200SHA3_ERR_INVALID_ARGUMENT;
+  if (!data) {  // fine only if every message is empty; checked before any work
+    for (uint64_t i = 0; i < count; ++i) {
+      if (lengths[i] != 0) return B200SHA3_ERR_INVALID_ARGUMENT;
+    }
+  }
 
-  std::vector<HostChunk> chunks;
   // average message size of a packed batch: the span from the first to the last message
   const uint64_t span = offsets[count - 1] + lengths[count - 1] - std::min(offsets[0], offsets[count - 1]);
-  const bool pipelined = (c.flags & B200SHA3_FLAG_NO_PIPELINE) == 0 &&
-                         plan_ordered_chunks(offsets, lengths, count,
-                                             chunk_target_bytes(span / count + digest_bytes), &chunks);
-  if (!pipelined) chunks.assign(1, whole_batch_chunk(offsets, lengths, count));
-  uint64_t max_span = 0, max_count = 0;
-  for (const HostChunk& ch : chunks) {
-    max_span = std::max(max_span, ch.hi - ch.lo);
-    max_count = std::max(max_count, ch.count);
-  }
-  if (max_span != 0 && !data) return B200SHA3_ERR_INVALID_ARGUMENT;
+  const bool pipelined = (c.flags & B200SHA3_FLAG_NO_PIPELINE) == 0;
+  ChunkPlanner planner(offsets, lengths, count, chunk_target_bytes(span / count + digest_bytes), pipelined);
 
   DeviceGuard guard;
   CU(guard.enter(c.device));
   tune_mempool_once();
   if (c.stream) CU(cudaStreamSynchronize(c.stream));
-  SlotPipeline pipe(static_cast<int>(std::min<size_t>(kPipelineSlots, chunks.size())),
-                    c.device_ms != nullptr);
+  SlotPipeline pipe(pipelined ? kPipelineSlots : 1, c.device_ms != nullptr);
   CU(pipe.init());
-  uint64_t total_span = 0;
-  for (const HostChunk& ch : chunks) total_span += ch.hi - ch.lo;
   HostIo io;
-  CU(io.init(data, total_span, digests, count * digest_bytes, offsets, 2 * count * sizeof(uint64_t)));
+  CU(io.init(data, span, digests, count * digest_bytes, offsets, 2 * count * sizeof(uint64_t)));
+  // per-slot device buffers, grown when a chunk needs more (chunks are near-equal, so this
+  // happens once per slot unless one message is huge)
   uint8_t* d_data[kPipelineSlots] = {};
   uint64_t* d_meta[kPipelineSlots] = {};  // offsets, then lengths
   uint8_t* d_out[kPipelineSlots] = {};
-  for (int s = 0; s < pipe.slots(); ++s) {
-    CU(pipe.alloc(s, &d_data[s], max_span));
-    CU(pipe.alloc(s, &d_meta[s], 2 * max_count * sizeof(uint64_t)));
-    CU(pipe.alloc(s, &d_out[s], max_count * digest_bytes));
-  }
+  uint64_t cap_data[kPipelineSlots] = {}, cap_count[kPipelineSlots] = {};
   int rc = B200SHA3_OK;
   uint32_t launches = 0;
-  for (size_t k = 0; k < chunks.size() && rc == B200SHA3_OK; ++k) {
+  HostChunk ch{};
+  for (size_t k = 0; rc == B200SHA3_OK && planner.next(&ch); ++k) {
     const int s = static_cast<int>(k % pipe.slots());
-    const HostChunk& ch = chunks[k];
     cudaStream_t stream = pipe.stream(s);
     cudaError_t e = cudaSuccess;
+    if (ch.hi - ch.lo > cap_data[s] || !d_data[s]) {
+      cap_data[s] = (ch.hi - ch.lo) + (ch.hi - ch.lo) / 8;
+      e = pipe.alloc(s, &d_data[s], cap_data[s]);
+    }
+    if (e == cudaSuccess && (ch.count > cap_count[s] || !d_meta[s])) {
+      cap_count[s] = ch.count + ch.count / 8;
+      e = pipe.alloc(s, &d_meta[s], 2 * cap_count[s] * sizeof(uint64_t));
+      if (e == cudaSuccess) e = pipe.alloc(s, &d_out[s], cap_count[s] * digest_bytes);
+    }
+    if (e != cudaSuccess) { rc = cuda_fail(e, "device staging allocation"); break; }
     if (ch.hi > ch.lo) {
       e = io.h2d(d_data[s], data + ch.lo, ch.hi - ch.lo, stream);
     }
@@ -348,12 +377,12 @@ int b200sha3_hash_batch(int algorithm, const uint8_t* data, const uint64_t* offs
       e = io.h2d_meta(d_meta[s], offsets + ch.first, ch.count * sizeof(uint64_t), stream);
     }
     if (e == cudaSuccess) {
-      e = io.h2d_meta(d_meta[s] + max_count, lengths + ch.first, ch.count * sizeof(uint64_t), stream);
+      e = io.h2d_meta(d_meta[s] + ch.count, lengths + ch.first, ch.count * sizeof(uint64_t), stream);
     }
     if (e == cudaSuccess) e = pipe.begin_kernels(s);
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D copy"); break; }
     // offsets are relative to `data`; the device copy starts at data + ch.lo
-    rc = run_batch_device(algorithm, d_data[s] - ch.lo, d_meta[s], d_meta[s] + max_count, ch.count,
+    rc = run_batch_device(algorithm, d_data[s] - ch.lo, d_meta[s], d_meta[s] + ch.count, ch.count,
                           xof_output_bits, digest_bytes, d_out[s], c, stream, &launches);
     if (rc != B200SHA3_OK) break;
     e = pipe.end_kernels(s);
