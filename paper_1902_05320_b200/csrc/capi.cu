@@ -135,11 +135,18 @@ int run_fixed_device(int algorithm, const uint8_t* d_data, uint64_t msg_len, uin
 int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_offsets,
                      const uint64_t* d_lengths, uint64_t count, uint64_t xof_bits,
                      uint64_t digest_bytes, uint8_t* d_digests, const Config& c,
-                     cudaStream_t stream, uint32_t* launches) {
+                     cudaStream_t stream, uint32_t* launches, const BatchHints* hints) {
   const Variant& v = kVariants[algorithm];
   tune_mempool_once();
   const uint64_t kSlice = 1ull << 30;
-  const bool bucketing = (c.flags & B200SHA3_FLAG_NO_BUCKETING) == 0;
+  const bool short_shape = c.kernel == B200SHA3_KERNEL_AUTO && is_aligned(d_data, 8) &&
+                           last_byte_mask(algorithm, xof_bits) == 0xffu &&
+                           short_supported(v.rate_lanes, digest_bytes);
+  // With host knowledge of the batch: all-short aligned batches go straight to the short
+  // kernel, equal-length ones straight to the generic kernel -- no classification, no order.
+  const bool host_short = hints && hints->all_short && hints->aligned8 && short_shape;
+  const bool host_plain = hints && !host_short && hints->all_equal && c.kernel != B200SHA3_KERNEL_STAGED;
+  const bool bucketing = (c.flags & B200SHA3_FLAG_NO_BUCKETING) == 0 && !host_short && !host_plain;
   for (uint64_t first = 0; first < count; first += kSlice) {
     const uint32_t n = static_cast<uint32_t>(std::min<uint64_t>(kSlice, count - first));
     uint32_t* scratch = nullptr;  // [0] unaligned flag, [1] ragged flag, then bucket scratch, then order
@@ -149,9 +156,17 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     uint32_t* bucket_scratch = scratch + 8;
     uint32_t* order = bucketing ? scratch + 8 + kBucketScratchWords : nullptr;
     CU(cudaMemsetAsync(flag, 0, 8 * sizeof(uint32_t), stream));
-    if (bucketing) {
+    // Batches of single-block messages only have their own kernel (kernel_short.cu).  Without
+    // host knowledge, whether this is one is known on the device only (flag words), so both
+    // kernels are launched and one of them returns at once.
+    const bool try_short = hints ? host_short : short_shape;
+    if (host_short) {
+      // flag words stay zero: "aligned, nothing long"
+    } else if (host_plain) {
+      if (!hints->aligned8) CU(cudaMemsetAsync(flag, 1, sizeof(uint32_t), stream));  // nonzero = unaligned
+    } else if (bucketing) {
       CU(launch_bucket_order(d_offsets + first, d_lengths + first, n, 8u * v.rate_lanes, order,
-                             bucket_scratch, flag, stream));
+                             bucket_scratch, flag, stream, try_short));
       if (launches) *launches += 3;
     } else {
       CU(launch_alignment_check(d_offsets + first, d_lengths + first, n, 8u * v.rate_lanes, flag, stream));
@@ -165,6 +180,8 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     args.order = order;
     args.unaligned_flag = is_aligned(d_data, 8) ? flag : nullptr;
     args.ragged_flag = flag + 1;
+    args.long_flag = flag + 2;
+    args.skip_if_short = (try_short && !host_short) ? 1u : 0u;
     args.aligned8 = 0u;  // used only when the base pointer itself is misaligned
     args.digests = d_digests + first * digest_bytes;
     args.digest_bytes = digest_bytes;
@@ -175,13 +192,20 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     plan.unroll = c.unroll;  // 0 = the kernel's default loop shape
     plan.fma_preset = c.fma_preset >= 0 ? c.fma_preset : kDefaultFmaGeneric;
     plan.block_threads = c.block_threads;
-    cudaError_t err = c.kernel == B200SHA3_KERNEL_STAGED ? launch_hash_staged(args, plan, stream)
-                                                         : launch_hash_generic(args, plan, stream);
+    cudaError_t err = cudaSuccess;
+    if (try_short) {
+      err = launch_hash_short(args, plan, stream);
+      if (err == cudaSuccess && launches) *launches += 1;
+    }
+    if (err == cudaSuccess && !host_short) {
+      err = c.kernel == B200SHA3_KERNEL_STAGED ? launch_hash_staged(args, plan, stream)
+                                               : launch_hash_generic(args, plan, stream);
+      if (err == cudaSuccess && launches) *launches += 1;
+    }
     if (err != cudaSuccess) {
       cudaFreeAsync(scratch, stream);
       return cuda_fail(err, "hash kernel launch");
     }
-    if (launches) *launches += 1;
     CU(cudaFreeAsync(scratch, stream));
   }
   return B200SHA3_OK;

@@ -145,11 +145,20 @@ int run_fixed_device(int algorithm, const uint8_t* d_data, uint64_t msg_len, uin
                      uint64_t xof_bits, uint64_t digest_bytes, uint8_t* d_digests,
                      const Config& c, cudaStream_t stream, uint32_t* launches);
 
+// What a caller that has read the offsets / lengths on the HOST (the host-buffer entries)
+// knows about a batch; lets run_batch_device pick the kernel without the device-side
+// classification / bucketing passes.
+struct BatchHints {
+  bool aligned8 = false;   // every message starts at a multiple of 8 (relative to `data`)
+  bool all_short = false;  // every message is shorter than the rate: single block
+  bool all_equal = false;  // all lengths are equal: nothing to bucket, uniform final block
+};
+
 // Variable-length batch already in HBM: bucketing pass (unless disabled) + hash kernel per
-// slice of at most 2^30 messages; asynchronous on `stream`.
+// slice of at most 2^30 messages; asynchronous on `stream`.  `hints` may be nullptr.
 int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_offsets,
                      const uint64_t* d_lengths, uint64_t count, uint64_t xof_bits,
                      uint64_t digest_bytes, uint8_t* d_digests, const Config& c,
-                     cudaStream_t stream, uint32_t* launches);
+                     cudaStream_t stream, uint32_t* launches, const BatchHints* hints = nullptr);
 
 }  // namespace b200sha3::capi

@@ -172,18 +172,28 @@ class SlotPipeline {
 struct HostChunk {
   uint64_t first, count;  // message range
   uint64_t lo, hi;        // byte range of `data` the chunk reads (lo is 16-byte aligned)
+  BatchHints hints;       // what the planner saw while reading the chunk's offsets / lengths
 };
 
 // One chunk holding the whole batch: the byte range [lo, hi) that its messages touch.
-HostChunk whole_batch_chunk(const uint64_t* offsets, const uint64_t* lengths, uint64_t count) {
-  uint64_t lo = ~0ull, hi = 0;
+HostChunk whole_batch_chunk(const uint64_t* offsets, const uint64_t* lengths, uint64_t count,
+                            uint64_t rate_bytes) {
+  uint64_t lo = ~0ull, hi = 0, misaligned = 0, max_len = 0;
+  bool equal = true;
   for (uint64_t i = 0; i < count; ++i) {
+    misaligned |= offsets[i];
+    max_len = std::max(max_len, lengths[i]);
+    equal = equal && lengths[i] == lengths[0];
     if (lengths[i] == 0) continue;
     lo = std::min(lo, offsets[i]);
     hi = std::max(hi, offsets[i] + lengths[i]);
   }
   if (hi == 0) lo = 0;
-  return HostChunk{0, count, lo & ~15ull, hi};  // device copy congruent to the host buffer mod 16
+  HostChunk ch{0, count, lo & ~15ull, hi, {}};  // device copy congruent to the host buffer mod 16
+  ch.hints.aligned8 = (misaligned & 7u) == 0;
+  ch.hints.all_short = max_len < rate_bytes;
+  ch.hints.all_equal = equal;
+  return ch;
 }
 
 // Chunks of a packed batch, planned one at a time while the previous ones are already in
@@ -195,46 +205,82 @@ HostChunk whole_batch_chunk(const uint64_t* offsets, const uint64_t* lengths, ui
 class ChunkPlanner {
  public:
   ChunkPlanner(const uint64_t* offsets, const uint64_t* lengths, uint64_t count, uint64_t target_bytes,
-               bool pipelined)
-      : offsets_(offsets), lengths_(lengths), count_(count), target_(target_bytes), pipelined_(pipelined) {}
+               uint64_t rate_bytes, bool pipelined)
+      : offsets_(offsets), lengths_(lengths), count_(count), target_(target_bytes), rate_(rate_bytes),
+        pipelined_(pipelined) {}
 
   bool next(HostChunk* out) {
     if (next_ >= count_) return false;
     if (!pipelined_) return rest(out);
-    HostChunk cur{next_, 0, 0, 0};
-    for (uint64_t i = next_; i < count_; ++i) {
-      const uint64_t end = offsets_[i] + lengths_[i];
+    HostChunk cur{next_, 0, 0, 0, {}};
+    uint64_t misaligned = 0, max_len = 0;
+    const uint64_t first_len = lengths_[next_];
+    bool equal = true;
+    const auto close = [&](uint64_t resume_at) {
+      cur.hints.aligned8 = (misaligned & 7u) == 0;
+      cur.hints.all_short = max_len < rate_;
+      cur.hints.all_equal = equal;
+      *out = cur;
+      next_ = resume_at;
+      return true;
+    };
+    // Strips of kStrip messages: the in-order test and the statistics of a strip are plain
+    // reductions without early exits (this loop reads 16 bytes per message and, for 2^24 short
+    // messages, is what the copy engines wait for); a strip that is not in order is walked
+    // message by message to find where the order breaks.
+    uint64_t i = next_;
+    while (i < count_) {
+      const uint64_t n = std::min<uint64_t>(kStrip, count_ - i);
+      const uint64_t* off = offsets_ + i;
+      const uint64_t* len = lengths_ + i;
+      uint64_t bad = (off[0] < prev_end_) | (off[0] + len[0] < off[0]);
+      uint64_t strip_or = off[0], strip_max = len[0], strip_ne = len[0] ^ first_len;
+      for (uint64_t k = 1; k < n; ++k) {
+        const uint64_t end_before = off[k - 1] + len[k - 1];
+        bad |= (off[k] < end_before) | (off[k] + len[k] < off[k]);
+        strip_or |= off[k];
+        strip_max = std::max(strip_max, len[k]);
+        strip_ne |= len[k] ^ first_len;
+      }
+      if (bad) break;  // handled below, message by message
+      if (cur.count == 0) cur.lo = off[0] & ~15ull;
+      cur.count += n;
+      cur.hi = off[n - 1] + len[n - 1];
+      prev_end_ = cur.hi;
+      misaligned |= strip_or;
+      max_len = std::max(max_len, strip_max);
+      equal = equal && strip_ne == 0;
+      i += n;
+      if (cur.hi - cur.lo >= target_ || cur.count >= (1ull << 22)) return close(i);
+    }
+    for (; i < count_; ++i) {  // only reached inside a strip that breaks the order
+      const uint64_t len = lengths_[i], end = offsets_[i] + len;
       if (offsets_[i] < prev_end_ || end < offsets_[i]) {  // out of order (or wrapping)
         if (cur.count == 0) return rest(out);
-        *out = cur;  // close the chunk in progress; the next call takes the rest
-        next_ = i;
-        return true;
+        return close(i);  // close the chunk in progress; the next call takes the rest
       }
       if (cur.count == 0) cur.lo = offsets_[i] & ~15ull;
       cur.count += 1;
       cur.hi = end;
       prev_end_ = end;
-      if (cur.hi - cur.lo >= target_ || cur.count >= (1ull << 22)) {
-        *out = cur;
-        next_ = i + 1;
-        return true;
-      }
+      misaligned |= offsets_[i];
+      max_len = std::max(max_len, len);
+      equal = equal && len == first_len;
     }
-    *out = cur;
-    next_ = count_;
-    return true;
+    return close(count_);
   }
 
  private:
   bool rest(HostChunk* out) {
-    *out = whole_batch_chunk(offsets_ + next_, lengths_ + next_, count_ - next_);
+    *out = whole_batch_chunk(offsets_ + next_, lengths_ + next_, count_ - next_, rate_);
     out->first = next_;
     next_ = count_;
     return true;
   }
   const uint64_t* offsets_;
   const uint64_t* lengths_;
-  uint64_t count_, target_;
+  static constexpr uint64_t kStrip = 1024;
+  uint64_t count_, target_, rate_;
   bool pipelined_;
   uint64_t next_ = 0, prev_end_ = 0;
 };
@@ -337,7 +383,8 @@ int b200sha3_hash_batch(int algorithm, const uint8_t* data, const uint64_t* offs
   // average message size of a packed batch: the span from the first to the last message
   const uint64_t span = offsets[count - 1] + lengths[count - 1] - std::min(offsets[0], offsets[count - 1]);
   const bool pipelined = (c.flags & B200SHA3_FLAG_NO_PIPELINE) == 0;
-  ChunkPlanner planner(offsets, lengths, count, chunk_target_bytes(span / count + digest_bytes), pipelined);
+  ChunkPlanner planner(offsets, lengths, count, chunk_target_bytes(span / count + digest_bytes),
+                       8u * kVariants[algorithm].rate_lanes, pipelined);
 
   DeviceGuard guard;
   CU(guard.enter(c.device));
@@ -383,7 +430,7 @@ int b200sha3_hash_batch(int algorithm, const uint8_t* data, const uint64_t* offs
     if (e != cudaSuccess) { rc = cuda_fail(e, "H2D copy"); break; }
     // offsets are relative to `data`; the device copy starts at data + ch.lo
     rc = run_batch_device(algorithm, d_data[s] - ch.lo, d_meta[s], d_meta[s] + ch.count, ch.count,
-                          xof_output_bits, digest_bytes, d_out[s], c, stream, &launches);
+                          xof_output_bits, digest_bytes, d_out[s], c, stream, &launches, &ch.hints);
     if (rc != B200SHA3_OK) break;
     e = pipe.end_kernels(s);
     if (e == cudaSuccess) {

@@ -68,7 +68,7 @@ bucket_histogram_kernel(const uint64_t* __restrict__ offsets,
   __syncthreads();
   const uint32_t base = blockIdx.x * (kBucketThreads * kBucketItems);
   const uint32_t first_tail = static_cast<uint32_t>(lengths[0] % rate_bytes);
-  uint32_t misaligned = 0u, ragged = 0u;
+  uint32_t misaligned = 0u, ragged = 0u, has_long = 0u;
 #pragma unroll
   for (int k = 0; k < kBucketItems; ++k) {
     const uint32_t i = base + k * kBucketThreads + threadIdx.x;
@@ -77,6 +77,7 @@ bucket_histogram_kernel(const uint64_t* __restrict__ offsets,
       atomicAdd(&local[bucket_key(len, rate_bytes)], 1u);
       misaligned |= static_cast<uint32_t>(offsets[i]) & 7u;
       ragged |= static_cast<uint32_t>(len % rate_bytes) ^ first_tail;
+      has_long |= len >= rate_bytes ? 1u : 0u;
     }
   }
   if (__any_sync(0xffffffffu, misaligned != 0u) && (threadIdx.x & 31) == 0) {
@@ -84,6 +85,9 @@ bucket_histogram_kernel(const uint64_t* __restrict__ offsets,
   }
   if (__any_sync(0xffffffffu, ragged != 0u) && (threadIdx.x & 31) == 0) {
     atomicOr(unaligned_flag + 1, 1u);
+  }
+  if (__any_sync(0xffffffffu, has_long != 0u) && (threadIdx.x & 31) == 0) {
+    atomicOr(unaligned_flag + 2, 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) {
@@ -112,7 +116,10 @@ bucket_scan_kernel(uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor) {
 __global__ void __launch_bounds__(kBucketThreads)
 bucket_scatter_kernel(const uint64_t* __restrict__ lengths, uint32_t count,
                       uint32_t rate_bytes, const uint32_t* __restrict__ bin_base,
-                      uint32_t* __restrict__ cursor, uint32_t* __restrict__ order) {
+                      uint32_t* __restrict__ cursor, uint32_t* __restrict__ order,
+                      const uint32_t* __restrict__ skip_flags) {
+  // an all-short, aligned batch goes to hash_short_kernel, which needs no order
+  if (skip_flags != nullptr && skip_flags[0] == 0u && skip_flags[2] == 0u) return;
   __shared__ uint32_t local[kBucketBins];   // per-block count, then block base
   for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) local[i] = 0u;
   __syncthreads();
@@ -143,11 +150,16 @@ __global__ void __launch_bounds__(256)
 alignment_check_kernel(const uint64_t* __restrict__ offsets, const uint64_t* __restrict__ lengths,
                        uint64_t count, uint32_t rate_bytes, uint32_t* __restrict__ unaligned_flag) {
   const uint32_t first_tail = static_cast<uint32_t>(lengths[0] % rate_bytes);
-  uint32_t misaligned = 0u, ragged = 0u;
+  uint32_t misaligned = 0u, ragged = 0u, has_long = 0u;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t len = lengths[i];
     misaligned |= static_cast<uint32_t>(offsets[i]) & 7u;
-    ragged |= static_cast<uint32_t>(lengths[i] % rate_bytes) ^ first_tail;
+    ragged |= static_cast<uint32_t>(len % rate_bytes) ^ first_tail;
+    has_long |= len >= rate_bytes ? 1u : 0u;
+  }
+  if (__any_sync(0xffffffffu, has_long != 0u) && (threadIdx.x & 31) == 0) {
+    atomicOr(unaligned_flag + 2, 1u);
   }
   if (__any_sync(0xffffffffu, misaligned != 0u) && (threadIdx.x & 31) == 0) {
     atomicOr(unaligned_flag, 1u);
@@ -241,7 +253,7 @@ cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream
 cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,
                                 uint32_t count, uint32_t rate_bytes, uint32_t* order,
                                 uint32_t* scratch, uint32_t* unaligned_flag,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, bool skip_order_if_short) {
   if (count == 0) return cudaSuccess;
   uint32_t* hist = scratch;
   uint32_t* cursor = scratch + kBucketBins;
@@ -253,8 +265,8 @@ cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths
                                                                 rate_bytes, hist,
                                                                 unaligned_flag);
   bucket_scan_kernel<<<1, kBucketBins, 0, stream>>>(hist, cursor);
-  bucket_scatter_kernel<<<blocks, kBucketThreads, 0, stream>>>(lengths, count, rate_bytes,
-                                                              hist, cursor, order);
+  bucket_scatter_kernel<<<blocks, kBucketThreads, 0, stream>>>(
+      lengths, count, rate_bytes, hist, cursor, order, skip_order_if_short ? unaligned_flag : nullptr);
   return cudaGetLastError();
 }
 

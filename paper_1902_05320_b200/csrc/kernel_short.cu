@@ -1,0 +1,77 @@
+// kernel_short.cu -- variable-length batches of SINGLE-BLOCK messages: every message shorter
+// than the rate (hashing keys, identifiers, short records of uneven length).
+//
+// The generic kernel serves such a batch at ~0.93 of the ALU roofline and ncu shows why: no
+// stalls, just instructions -- a rolled permutation that cannot drop the work on the capacity
+// lanes (zero before the first permutation) or on the lanes nobody reads after the last one,
+// the block-count loop, the processing order.  When the classification pass
+// (kernel_aux.cu) finds 8-byte aligned starts and no message of a whole block, this kernel
+// does the batch instead: predicated lane loads straight into a zero state
+// (absorb_tail, ragged form), the peeled permutation of the one-block kernel
+// (1 + 7x3 + 2 rounds), OW digest words out, input order.  It is launched next to the
+// generic kernel; each of the two returns at once when the flags give the batch to the other.
+#include "kernels.cuh"
+#include "sponge.cuh"
+
+namespace b200sha3 {
+
+namespace {
+
+template <int RL, int OW>
+__global__ void __launch_bounds__(256)
+hash_short_kernel(const HashArgs args) {
+  static_assert(OW <= 2 * RL, "digest must fit one block");
+  if (*args.unaligned_flag != 0u || *args.long_flag != 0u) return;  // the generic kernel's batch
+  // (A persistent grid-stride form of this kernel was measured 4 % slower on its own batches:
+  // 0.921 vs 0.957 of the roofline on 2^24 x 0..135 B.)
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (tid >= args.count) return;
+  const uint8_t* p = args.data + args.offsets[tid];
+  const uint32_t len = static_cast<uint32_t>(args.lengths[tid]);  // < 8 * RL
+  State a;
+  state_zero(a);
+  absorb_tail<RL>(a, p, len, args.head, /*aligned8=*/true, /*ragged=*/true);
+  keccak_f1600<23, 0u>(a);  // peeled 1 + 7x3 + 2
+  emit_block<RL>(a, args.digests + tid * (4u * OW), 4u * OW);
+}
+
+template <int RL, int OW>
+cudaError_t launch_instance(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {
+  const int threads = plan.block_threads > 0 ? plan.block_threads : 128;
+  const uint64_t blocks = (args.count + threads - 1) / threads;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+  hash_short_kernel<RL, OW><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(args);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// The four hashes at their digest size; the two SHAKEs at 128-, 256- and 512-bit outputs.
+bool short_supported(int rate_lanes, uint64_t digest_bytes) {
+  switch (rate_lanes) {
+    case 18: return digest_bytes == 28;
+    case 17: return digest_bytes == 32 || digest_bytes == 16 || digest_bytes == 64;
+    case 13: return digest_bytes == 48;
+    case 9: return digest_bytes == 64;
+    case 21: return digest_bytes == 16 || digest_bytes == 32 || digest_bytes == 64;
+    default: return false;
+  }
+}
+
+cudaError_t launch_hash_short(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {
+  if (!short_supported(plan.rate_lanes, args.digest_bytes) || !args.offsets || !args.lengths ||
+      !args.unaligned_flag || !args.long_flag || args.last_mask != 0xffu) {
+    return cudaErrorNotSupported;
+  }
+  const int ow = static_cast<int>(args.digest_bytes / 4);
+#define B200SHA3_SHORT(RL, OW) \
+  if (plan.rate_lanes == RL && ow == OW) return launch_instance<RL, OW>(args, plan, stream);
+  B200SHA3_SHORT(18, 7) B200SHA3_SHORT(17, 8) B200SHA3_SHORT(13, 12) B200SHA3_SHORT(9, 16)
+  B200SHA3_SHORT(17, 4) B200SHA3_SHORT(17, 16) B200SHA3_SHORT(21, 4) B200SHA3_SHORT(21, 8)
+  B200SHA3_SHORT(21, 16)
+#undef B200SHA3_SHORT
+  return cudaErrorNotSupported;
+}
+
+}  // namespace b200sha3

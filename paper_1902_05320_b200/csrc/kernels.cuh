@@ -19,6 +19,10 @@ struct HashArgs {
                                    // 8-byte aligned; nullptr: use `aligned8`
   const uint32_t* ragged_flag;     // device word, nonzero if the final (partial) blocks of the
                                    // batch differ in length; nullptr: they are all alike
+  const uint32_t* long_flag;       // device word, nonzero if some message fills a whole rate block
+                                   // (>= rate bytes); nullptr: unknown
+  uint32_t skip_if_short;          // generic kernel: leave the batch to hash_short_kernel when it
+                                   // is all-short and aligned (the flags above say so)
   uint8_t* digests;          // count * digest_bytes, message order
   uint64_t digest_bytes;
   uint32_t head;             // pad head byte: 0x06 / 0x1f
@@ -63,6 +67,13 @@ cudaError_t launch_hash_oneblock(const HashArgs& args, const LaunchPlan& plan,
                                  cudaStream_t stream);
 bool oneblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
 
+// Variable-length batches made of single-block messages only (kernel_short.cu): one launch
+// that does the work when the flag words say "8-byte aligned starts, no message reaches the
+// rate" and returns at once otherwise (the generic kernel, launched next with skip_if_short,
+// makes the opposite choice).  cudaErrorNotSupported when no instantiation matches.
+cudaError_t launch_hash_short(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
+bool short_supported(int rate_lanes, uint64_t digest_bytes);
+
 // Lane-split kernel (5 threads per state, warp shuffles); equal-length,
 // 8-byte aligned, single-block messages.
 cudaError_t launch_hash_lanesplit(const HashArgs& args, const LaunchPlan& plan,
@@ -77,15 +88,17 @@ cudaError_t launch_hash_staged(const HashArgs& args, const LaunchPlan& plan, cud
 cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream);
 
 // Bucketing by block count: writes a processing order (heaviest first), sets
-// *unaligned_flag if any offset is not a multiple of 8 and unaligned_flag[1] (the "ragged"
-// word) if the messages do not all leave the same number of bytes for the final block.
+// *unaligned_flag if any offset is not a multiple of 8, unaligned_flag[1] (the "ragged"
+// word) if the messages do not all leave the same number of bytes for the final block and
+// unaligned_flag[2] (the "long" word) if some message is at least one rate block long -- in
+// which case only the ordering is computed at all.
 // `scratch` needs kBucketScratchWords 32-bit words.
 constexpr int kBucketBins = 256;
 constexpr int kBucketScratchWords = 2 * kBucketBins + 8;
 cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,
                                 uint32_t count, uint32_t rate_bytes, uint32_t* order,
                                 uint32_t* scratch, uint32_t* unaligned_flag,
-                                cudaStream_t stream);
+                                cudaStream_t stream, bool skip_order_if_short = false);
 // The two flag words only (no ordering).
 cudaError_t launch_alignment_check(const uint64_t* offsets, const uint64_t* lengths, uint64_t count,
                                    uint32_t rate_bytes, uint32_t* unaligned_flag, cudaStream_t stream);

@@ -553,3 +553,34 @@ def test_pageable_host_buffers_are_staged_through_the_bounce_ring(engine, oracle
     for i in rng.choice(count, 200, replace=False):
         m = data[int(offsets[i]):int(offsets[i] + lengths[i])].tobytes()
         assert host[i].tobytes() == oracle.hash_one(5, m, 264)
+
+
+@pytest.mark.parametrize("algorithm,bits", [(0, 0), (1, 0), (2, 0), (3, 0), (4, 128), (4, 256), (4, 512),
+                                            (5, 128), (5, 256), (5, 512), (4, 328), (5, 1600)])
+def test_all_short_ragged_batches(engine, oracle, algorithm, bits):
+    """Variable-length batches in which every message is shorter than the rate go to
+    hash_short_kernel (csrc/kernel_short.cu) when the starts are 8-byte aligned -- a choice made
+    on the device from the classification flags.  Every length 0..rate-1 several times over, both
+    layouts (aligned: short kernel; packed back to back: generic kernel), digest slots at an odd
+    address, XOF lengths with and without an instantiation, and the same batch with one
+    whole-block message appended (generic kernel) must all match the oracle."""
+    import torch
+    rate = oracle.rate_bytes(algorithm)
+    rng = np.random.default_rng(100 + algorithm)
+    lengths = np.concatenate([np.arange(rate), rng.integers(0, rate, 3000)]).astype(np.uint64)
+    rng.shuffle(lengths)
+    for align, extra in ((8, None), (1, None), (8, rate), (8, 5 * rate + 3)):
+        lens = lengths if extra is None else np.concatenate([lengths, [np.uint64(extra)]]).astype(np.uint64)
+        padded = (lens + np.uint64(align - 1)) // np.uint64(align) * np.uint64(align)
+        offsets = (np.cumsum(padded) - padded).astype(np.uint64)
+        data = rng.integers(0, 256, int(padded.sum()) + 16, dtype=np.uint8)
+        expect = oracle.hash_batch(algorithm, data, offsets, lens, xof_bits=bits, workers=8)
+        nbytes = expect.shape[1]
+        d_out = torch.zeros(len(lens) * nbytes + 3, dtype=torch.uint8, device="cuda")
+        for shift in (0, 3):    # digest array 16-byte aligned, then at an odd address
+            out = d_out[shift:shift + len(lens) * nbytes].view(len(lens), nbytes)
+            got = engine.hash_batch(algorithm, torch.from_numpy(data).cuda(), torch.from_numpy(offsets).cuda(),
+                                    torch.from_numpy(lens).cuda(), bits, out=out)
+            assert (got.cpu().numpy() == expect).all(), (align, extra, shift)
+        host = engine.hash_batch(algorithm, data, offsets, lens, bits)      # host entry, same batch
+        assert (host == expect).all(), (align, extra, "host")
