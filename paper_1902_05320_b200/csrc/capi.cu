@@ -144,7 +144,7 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
                            short_supported(v.rate_lanes, digest_bytes);
   // With host knowledge of the batch: all-short aligned batches go straight to the short
   // kernel, equal-length ones straight to the generic kernel -- no classification, no order.
-  const bool host_short = hints && hints->all_short && hints->aligned8 && short_shape;
+  const bool host_short = hints && hints->all_short && short_shape;
   const bool host_plain = hints && !host_short && hints->all_equal && c.kernel != B200SHA3_KERNEL_STAGED;
   const bool bucketing = (c.flags & B200SHA3_FLAG_NO_BUCKETING) == 0 && !host_short && !host_plain;
   for (uint64_t first = 0; first < count; first += kSlice) {
@@ -160,8 +160,8 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     // host knowledge, whether this is one is known on the device only (flag words), so both
     // kernels are launched and one of them returns at once.
     const bool try_short = hints ? host_short : short_shape;
-    if (host_short) {
-      // flag words stay zero: "aligned, nothing long"
+    if (host_short) {  // "nothing long" (word 2 stays zero); word 0 says whether the starts are aligned
+      if (!hints->aligned8) CU(cudaMemsetAsync(flag, 1, sizeof(uint32_t), stream));
     } else if (host_plain) {
       if (!hints->aligned8) CU(cudaMemsetAsync(flag, 1, sizeof(uint32_t), stream));  // nonzero = unaligned
     } else if (bucketing) {

@@ -118,8 +118,8 @@ bucket_scatter_kernel(const uint64_t* __restrict__ lengths, uint32_t count,
                       uint32_t rate_bytes, const uint32_t* __restrict__ bin_base,
                       uint32_t* __restrict__ cursor, uint32_t* __restrict__ order,
                       const uint32_t* __restrict__ skip_flags) {
-  // an all-short, aligned batch goes to hash_short_kernel, which needs no order
-  if (skip_flags != nullptr && skip_flags[0] == 0u && skip_flags[2] == 0u) return;
+  // an all-short batch goes to hash_short_kernel, which needs no order
+  if (skip_flags != nullptr && skip_flags[2] == 0u) return;
   __shared__ uint32_t local[kBucketBins];   // per-block count, then block base
   for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) local[i] = 0u;
   __syncthreads();

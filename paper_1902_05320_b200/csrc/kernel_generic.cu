@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(256, 2)
 hash_generic_kernel(const HashArgs args) {
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (tid >= args.count) return;
-  if (args.skip_if_short != 0u && *args.unaligned_flag == 0u && *args.long_flag == 0u) {
+  if (args.skip_if_short != 0u && *args.long_flag == 0u) {
     return;  // hash_short_kernel has this batch
   }
   const uint64_t m = args.order ? static_cast<uint64_t>(args.order[tid]) : tid;

@@ -5,8 +5,8 @@
 // stalls, just instructions -- a rolled permutation that cannot drop the work on the capacity
 // lanes (zero before the first permutation) or on the lanes nobody reads after the last one,
 // the block-count loop, the processing order.  When the classification pass
-// (kernel_aux.cu) finds 8-byte aligned starts and no message of a whole block, this kernel
-// does the batch instead: predicated lane loads straight into a zero state
+// (kernel_aux.cu) finds no message of a whole block, this kernel does the batch instead
+// (8-byte aligned starts: 8-byte loads; any other layout: aligned 4-byte loads + PRMT): predicated lane loads straight into a zero state
 // (absorb_tail, ragged form), the peeled permutation of the one-block kernel
 // (1 + 7x3 + 2 rounds), OW digest words out, input order.  It is launched next to the
 // generic kernel; each of the two returns at once when the flags give the batch to the other.
@@ -21,7 +21,8 @@ template <int RL, int OW>
 __global__ void __launch_bounds__(256)
 hash_short_kernel(const HashArgs args) {
   static_assert(OW <= 2 * RL, "digest must fit one block");
-  if (*args.unaligned_flag != 0u || *args.long_flag != 0u) return;  // the generic kernel's batch
+  if (*args.long_flag != 0u) return;  // the generic kernel's batch
+  const bool aligned8 = *args.unaligned_flag == 0u;  // else: 4-byte loads re-assembled with PRMT
   // (A persistent grid-stride form of this kernel was measured 4 % slower on its own batches:
   // 0.921 vs 0.957 of the roofline on 2^24 x 0..135 B.)
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -30,7 +31,7 @@ hash_short_kernel(const HashArgs args) {
   const uint32_t len = static_cast<uint32_t>(args.lengths[tid]);  // < 8 * RL
   State a;
   state_zero(a);
-  absorb_tail<RL>(a, p, len, args.head, /*aligned8=*/true, /*ragged=*/true);
+  absorb_tail<RL>(a, p, len, args.head, aligned8, /*ragged=*/true);
   keccak_f1600<23, 0u>(a);  // peeled 1 + 7x3 + 2
   emit_block<RL>(a, args.digests + tid * (4u * OW), 4u * OW);
 }

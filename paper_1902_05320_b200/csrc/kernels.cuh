@@ -22,7 +22,7 @@ struct HashArgs {
   const uint32_t* long_flag;       // device word, nonzero if some message fills a whole rate block
                                    // (>= rate bytes); nullptr: unknown
   uint32_t skip_if_short;          // generic kernel: leave the batch to hash_short_kernel when it
-                                   // is all-short and aligned (the flags above say so)
+                                   // is all-short (the flag above says so)
   uint8_t* digests;          // count * digest_bytes, message order
   uint64_t digest_bytes;
   uint32_t head;             // pad head byte: 0x06 / 0x1f
@@ -68,8 +68,8 @@ cudaError_t launch_hash_oneblock(const HashArgs& args, const LaunchPlan& plan,
 bool oneblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
 
 // Variable-length batches made of single-block messages only (kernel_short.cu): one launch
-// that does the work when the flag words say "8-byte aligned starts, no message reaches the
-// rate" and returns at once otherwise (the generic kernel, launched next with skip_if_short,
+// that does the work when the flag words say "no message reaches the rate" and returns at
+// once otherwise (the generic kernel, launched next with skip_if_short,
 // makes the opposite choice).  cudaErrorNotSupported when no instantiation matches.
 cudaError_t launch_hash_short(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
 bool short_supported(int rate_lanes, uint64_t digest_bytes);
