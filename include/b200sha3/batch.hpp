@@ -37,8 +37,9 @@ enum class Algorithm { sha3_224, sha3_256, sha3_384, sha3_512, shake128, shake25
 enum class Backend { sequential, parallel };
 
 // proj/core/include/sha3/batch.hpp:15-19.  On the GPU engine `workers` sizes the
-// host-side pack/unpack thread pool (0 = one per hardware thread); `backend`
-// and `chunk_size` have no device meaning and are accepted for compatibility.
+// host-side pack/unpack thread pool (0 = one per hardware thread) and
+// Backend::sequential keeps all host work on the calling thread; `chunk_size`
+// has no device meaning and is accepted for compatibility.
 struct EngineConfig {
   Backend backend = Backend::parallel;
   unsigned workers = 0;

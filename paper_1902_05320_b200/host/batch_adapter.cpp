@@ -25,6 +25,7 @@ namespace sha3::b200 {
 namespace {
 
 unsigned pack_workers(const EngineConfig& config) {  // like resolve_workers, batch.cpp:38-44
+  if (config.backend == Backend::sequential) return 1;  // the caller's thread only (batch.cpp:86-89)
   if (config.workers > 0) return config.workers;
   const unsigned hw = std::thread::hardware_concurrency();
   return hw > 0 ? hw : 1;
