@@ -317,7 +317,8 @@ class BatchPipeline {
       const int n = env ? std::atoi(env) : 0;
       return n >= 1 && n <= 8 ? n : kLanesPerDevice;
     }();
-    for (int rep = 0; rep < lanes_per_device; ++rep) {
+    const int reps = workers_ == 1 ? 1 : lanes_per_device;  // one worker: no second thread at all
+    for (int rep = 0; rep < reps; ++rep) {
       if (device_.devices.empty()) lanes_.push_back(device_.device);
       for (int d : device_.devices) lanes_.push_back(d);
     }
