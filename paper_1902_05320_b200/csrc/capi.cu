@@ -75,12 +75,18 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
 
   const bool fits_oneblock = oneblock_supported(v.rate_lanes, msg_len, digest_bytes) &&
                              is_aligned(d_data, 16) && is_aligned(d_digests, 16);
+  // single-block lengths the one-block kernel has no shape for (10, 20, 100 bytes ...)
+  const bool fits_short = !fits_oneblock && c.kernel == B200SHA3_KERNEL_AUTO &&
+                          msg_len < 8u * static_cast<uint64_t>(v.rate_lanes) &&
+                          args.last_mask == 0xffu && short_supported(v.rate_lanes, digest_bytes);
   int kernel = c.kernel;
   if (kernel == B200SHA3_KERNEL_AUTO) {
     kernel = fits_oneblock ? B200SHA3_KERNEL_ONEBLOCK : B200SHA3_KERNEL_GENERIC;
   }
   cudaError_t err;
-  if (kernel == B200SHA3_KERNEL_ONEBLOCK) {
+  if (fits_short) {
+    err = launch_hash_short_fixed(args, plan, stream);
+  } else if (kernel == B200SHA3_KERNEL_ONEBLOCK) {
     if (!fits_oneblock) {
       set_error_text("one-block kernel does not fit this batch");
       return B200SHA3_ERR_UNSUPPORTED;

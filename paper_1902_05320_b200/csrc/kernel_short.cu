@@ -36,6 +36,41 @@ hash_short_kernel(const HashArgs args) {
   emit_block<RL>(a, args.digests + tid * (4u * OW), 4u * OW);
 }
 
+// The same for EQUAL-LENGTH batches of any length below the rate -- what the one-block kernel
+// (whole lanes of 32 / 64 / 128 bytes, 16-byte aligned) does not take: the paper's own 10-byte
+// messages, 20- or 100-byte records.  The length is uniform, so both tail forms
+// are jump tables without divergence: whole-lane loads when every start is 8-byte aligned,
+// aligned 4-byte loads + PRMT otherwise.
+template <int RL, int OW>
+__global__ void __launch_bounds__(256)
+hash_short_fixed_kernel(const uint8_t* __restrict__ data, uint8_t* __restrict__ digests, uint64_t count,
+                        uint32_t len, uint32_t head, uint32_t aligned8) {
+  static_assert(OW <= 2 * RL, "digest must fit one block");
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (tid >= count) return;
+  const uint8_t* p = data + tid * len;
+  State a;
+  state_zero(a);
+  if (aligned8 != 0u) {
+    absorb_tail<RL>(a, p, len, head, /*aligned8=*/true, /*ragged=*/false);
+  } else {
+    absorb_tail_uniform_unaligned<RL>(a, p, len, head);
+  }
+  keccak_f1600<23, 0u>(a);  // peeled 1 + 7x3 + 2
+  emit_block<RL>(a, digests + tid * (4u * OW), 4u * OW);
+}
+
+template <int RL, int OW>
+cudaError_t launch_fixed_instance(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {
+  const int threads = plan.block_threads > 0 ? plan.block_threads : 128;
+  const uint64_t blocks = (args.count + threads - 1) / threads;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+  hash_short_fixed_kernel<RL, OW><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
+      args.data, args.digests, args.count, static_cast<uint32_t>(args.fixed_len), args.head, args.aligned8);
+  return cudaGetLastError();
+}
+
 template <int RL, int OW>
 cudaError_t launch_instance(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {
   const int threads = plan.block_threads > 0 ? plan.block_threads : 128;
@@ -58,6 +93,21 @@ bool short_supported(int rate_lanes, uint64_t digest_bytes) {
     case 21: return digest_bytes == 16 || digest_bytes == 32 || digest_bytes == 64;
     default: return false;
   }
+}
+
+cudaError_t launch_hash_short_fixed(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {
+  if (!short_supported(plan.rate_lanes, args.digest_bytes) || args.offsets || args.lengths || args.order ||
+      args.fixed_len >= 8u * static_cast<uint64_t>(plan.rate_lanes) || args.last_mask != 0xffu) {
+    return cudaErrorNotSupported;
+  }
+  const int ow = static_cast<int>(args.digest_bytes / 4);
+#define B200SHA3_SHORT(RL, OW) \
+  if (plan.rate_lanes == RL && ow == OW) return launch_fixed_instance<RL, OW>(args, plan, stream);
+  B200SHA3_SHORT(18, 7) B200SHA3_SHORT(17, 8) B200SHA3_SHORT(13, 12) B200SHA3_SHORT(9, 16)
+  B200SHA3_SHORT(17, 4) B200SHA3_SHORT(17, 16) B200SHA3_SHORT(21, 4) B200SHA3_SHORT(21, 8)
+  B200SHA3_SHORT(21, 16)
+#undef B200SHA3_SHORT
+  return cudaErrorNotSupported;
 }
 
 cudaError_t launch_hash_short(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {

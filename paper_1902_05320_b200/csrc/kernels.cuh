@@ -73,6 +73,8 @@ bool oneblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes)
 // makes the opposite choice).  cudaErrorNotSupported when no instantiation matches.
 cudaError_t launch_hash_short(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
 bool short_supported(int rate_lanes, uint64_t digest_bytes);
+// Equal-length form: any length below the rate (args.fixed_len), any alignment (args.aligned8).
+cudaError_t launch_hash_short_fixed(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
 
 // Lane-split kernel (5 threads per state, warp shuffles); equal-length,
 // 8-byte aligned, single-block messages.

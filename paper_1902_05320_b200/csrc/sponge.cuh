@@ -162,6 +162,64 @@ __device__ __forceinline__ void absorb_tail(State& a, const uint8_t* p, uint32_t
   a.hi[RL - 1] ^= 0x80000000u;
 }
 
+// Final block of an EQUAL-LENGTH batch whose messages do not start on 8-byte boundaries (the
+// paper's 10-byte messages: message i starts at 10 i).  `rem` = W whole 32-bit
+// words + rb bytes is the same in every thread, so a jump table over W gives each case
+// statically indexed aligned 4-byte loads and PRMTs with no predicates, except on the last two
+// aligned words, which hold message bytes only for some shifts `sh` (the shift differs from
+// thread to thread).  Nothing is read outside the aligned words that hold message bytes.
+template <int RL, int W>
+__device__ __forceinline__ void absorb_tail_uniform_case(State& a, const uint32_t* q, uint32_t sel,
+                                                         uint32_t sh, uint32_t rb, uint32_t head) {
+  if constexpr (W < 2 * RL) {
+    // aligned word k covers message bytes [4k - sh, 4k - sh + 4): k < W always holds some,
+    // k = W iff rb + sh > 0 (W = 0: iff rb > 0 -- an empty message touches nothing),
+    // k = W + 1 iff rb + sh > 4
+    uint32_t al[W + 2];
+#pragma unroll
+    for (int k = 0; k < W; ++k) al[k] = ld_u32(q + k);
+    al[W] = ((W == 0 ? rb : rb + sh) > 0u) ? ld_u32(q + W) : 0u;
+    al[W + 1] = (rb + sh > 4u) ? ld_u32(q + W + 1) : 0u;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      const uint32_t w = __byte_perm(al[j], al[j + 1], sel);
+      if (j & 1) {
+        a.hi[j >> 1] ^= w;
+      } else {
+        a.lo[j >> 1] ^= w;
+      }
+    }
+    const uint32_t t = (__byte_perm(al[W], al[W + 1], sel) & ((1u << (8u * rb)) - 1u)) | (head << (8u * rb));
+    if (W & 1) {
+      a.hi[W >> 1] ^= t;
+    } else {
+      a.lo[W >> 1] ^= t;
+    }
+  }
+}
+
+template <int RL>
+__device__ __forceinline__ void absorb_tail_uniform_unaligned(State& a, const uint8_t* p, uint32_t rem,
+                                                              uint32_t head) {
+  const uint32_t sh = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(p)) & 3u;
+  const uint32_t* q = reinterpret_cast<const uint32_t*>(p - sh);
+  const uint32_t sel = 0x3210u + 0x1111u * sh;
+  const uint32_t rb = rem & 3u;
+  switch (rem >> 2) {
+#define B200SHA3_UTAIL_CASE(W) \
+  case W: absorb_tail_uniform_case<RL, W>(a, q, sel, sh, rb, head); break;
+#define B200SHA3_UTAIL_CASES6(W)                                                    \
+  B200SHA3_UTAIL_CASE(W) B200SHA3_UTAIL_CASE(W + 1) B200SHA3_UTAIL_CASE(W + 2)      \
+  B200SHA3_UTAIL_CASE(W + 3) B200SHA3_UTAIL_CASE(W + 4) B200SHA3_UTAIL_CASE(W + 5)
+    B200SHA3_UTAIL_CASES6(0) B200SHA3_UTAIL_CASES6(6) B200SHA3_UTAIL_CASES6(12) B200SHA3_UTAIL_CASES6(18)
+    B200SHA3_UTAIL_CASES6(24) B200SHA3_UTAIL_CASES6(30) B200SHA3_UTAIL_CASES6(36)
+#undef B200SHA3_UTAIL_CASES6
+#undef B200SHA3_UTAIL_CASE
+    default: break;
+  }
+  a.hi[RL - 1] ^= 0x80000000u;
+}
+
 __device__ __forceinline__ uint32_t state_word(const State& a, int j) {
   return (j & 1) ? a.hi[j >> 1] : a.lo[j >> 1];
 }

@@ -584,3 +584,27 @@ def test_all_short_ragged_batches(engine, oracle, algorithm, bits):
             assert (got.cpu().numpy() == expect).all(), (align, extra, shift)
         host = engine.hash_batch(algorithm, data, offsets, lens, bits)      # host entry, same batch
         assert (host == expect).all(), (align, extra, "host")
+
+
+@pytest.mark.parametrize("algorithm,bits", [(0, 0), (1, 0), (2, 0), (3, 0), (4, 256), (5, 512), (5, 128), (4, 1000)])
+def test_equal_length_single_block_batches_of_every_length(engine, oracle, algorithm, bits):
+    """Equal-length batches of every length 0 .. rate-1 (the paper's 10-byte messages among them,
+    PAPER.md:307): lengths that are not 32 / 64 / 128 bytes go to hash_short_fixed_kernel
+    (csrc/kernel_short.cu) with its uniform jump-table tails -- whole-lane loads when every
+    start is 8-byte aligned, 4-byte loads + PRMT otherwise.  Device entry at three base
+    alignments and the host entry, against the oracle."""
+    import torch
+    rate = oracle.rate_bytes(algorithm)
+    rng = np.random.default_rng(200 + algorithm)
+    count = 257
+    for msg_len in range(rate):
+        data = rng.integers(0, 256, count * msg_len + 24, dtype=np.uint8)
+        for lead in (0, 1, 4) if msg_len % 5 == 0 else (0,):
+            view = data[lead:lead + count * msg_len]
+            expect = oracle.hash_batch(algorithm, view, fixed_len=msg_len, count=count, xof_bits=bits, workers=4)
+            dev = torch.from_numpy(data).cuda()[lead:lead + max(count * msg_len, 1)]
+            got = engine.hash_fixed(algorithm, dev, msg_len, count, bits).cpu().numpy()
+            assert (got == expect).all(), (msg_len, lead)
+        host = engine.hash_fixed(algorithm, data[:max(count * msg_len, 1)], msg_len, count, bits)
+        assert (host == oracle.hash_batch(algorithm, data[:count * msg_len], fixed_len=msg_len, count=count,
+                                          xof_bits=bits, workers=4)).all(), (msg_len, "host")
