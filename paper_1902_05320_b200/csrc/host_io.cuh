@@ -11,9 +11,33 @@
 #include <thread>
 #include <vector>
 
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
+
 #include "capi_common.cuh"
 
 namespace b200sha3::capi {
+
+// memcpy whose destination is written once here and read once by a copy engine (a pinned
+// bounce block): whole cache lines go out with streaming stores -- no read-for-ownership.
+inline void copy_for_dma(uint8_t* dst, const uint8_t* src, size_t n) {
+#if defined(__SSE2__)
+  const size_t head = (64 - reinterpret_cast<uintptr_t>(dst) % 64) % 64;
+  if (n >= 4096 && head < n) {
+    if (head) std::memcpy(dst, src, head);
+    const size_t body = (n - head) & ~size_t{63};
+    for (size_t b = 0; b < body; b += 16) {
+      _mm_stream_si128(reinterpret_cast<__m128i*>(dst + head + b),
+                       _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + head + b)));
+    }
+    if (head + body < n) std::memcpy(dst + head + body, src + head + body, n - head - body);
+    _mm_sfence();
+    return;
+  }
+#endif
+  std::memcpy(dst, src, n);
+}
 
 // ---- pageable host memory ----------------------------------------------------------------
 // cudaMemcpyAsync on pageable memory is staged by the driver through one thread: 8-10 GB/s
@@ -61,9 +85,14 @@ class CopyPool {
     for (auto& t : threads_) t.join();
   }
 
-  void copy(void* dst, const void* src, size_t bytes) {
+  // `for_dma`: dst is a pinned block the copy engine reads next (streaming stores)
+  void copy(void* dst, const void* src, size_t bytes, bool for_dma = false) {
     if (threads_.empty() || bytes < min_parallel_) {
-      std::memcpy(dst, src, bytes);
+      if (for_dma) {
+        copy_for_dma(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes);
+      } else {
+        std::memcpy(dst, src, bytes);
+      }
       return;
     }
     {
@@ -71,6 +100,7 @@ class CopyPool {
       dst_ = static_cast<uint8_t*>(dst);
       src_ = static_cast<const uint8_t*>(src);
       bytes_ = bytes;
+      for_dma_ = for_dma;
       const size_t parts = threads_.size() + 1;
       piece_ = ((bytes + parts - 1) / parts + 4095) & ~size_t{4095};
       pending_ = threads_.size();
@@ -85,7 +115,12 @@ class CopyPool {
  private:
   void copy_piece(size_t index) {
     const size_t lo = std::min(bytes_, index * piece_), hi = std::min(bytes_, lo + piece_);
-    if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+    if (hi <= lo) return;
+    if (for_dma_) {
+      copy_for_dma(dst_ + lo, src_ + lo, hi - lo);
+    } else {
+      std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+    }
   }
   void worker(size_t index) {
     uint64_t seen = 0;
@@ -110,6 +145,7 @@ class CopyPool {
   uint8_t* dst_ = nullptr;
   const uint8_t* src_ = nullptr;
   size_t bytes_ = 0, piece_ = 0, pending_ = 0;
+  bool for_dma_ = false;
 };
 
 // The pinned bounce ring of one calling thread: kSlots blocks of kBlock bytes, used round-robin
@@ -144,7 +180,7 @@ class BounceRing {
       int slot = 0;
       cudaError_t e = acquire(&slot, pool);
       if (e != cudaSuccess) return e;
-      pool.copy(block(slot), static_cast<const uint8_t*>(src) + off, n);
+      pool.copy(block(slot), static_cast<const uint8_t*>(src) + off, n, /*for_dma=*/true);
       e = cudaMemcpyAsync(static_cast<uint8_t*>(dst) + off, block(slot), n, cudaMemcpyHostToDevice, stream);
       if (e == cudaSuccess) e = cudaEventRecord(events_[slot], stream);
       if (e != cudaSuccess) return e;
