@@ -73,7 +73,10 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
   plan.rate_lanes = v.rate_lanes;
   plan.block_threads = c.block_threads;
 
-  const bool fits_oneblock = oneblock_supported(v.rate_lanes, msg_len, digest_bytes) &&
+  // The one-block and lane-split kernels write whole words and never see last_mask: an XOF
+  // length that is not a whole number of bytes (batch.cpp:22-24) goes to the generic kernel.
+  const bool whole_bytes = args.last_mask == 0xffu;
+  const bool fits_oneblock = whole_bytes && oneblock_supported(v.rate_lanes, msg_len, digest_bytes) &&
                              is_aligned(d_data, 16) && is_aligned(d_digests, 16);
   // single-block lengths the one-block kernel has no shape for (10, 20, 100 bytes ...)
   const bool fits_short = !fits_oneblock && c.kernel == B200SHA3_KERNEL_AUTO &&
@@ -96,7 +99,7 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
     args.aligned8 = 1u;
     err = launch_hash_oneblock(args, plan, stream);
   } else if (kernel == B200SHA3_KERNEL_LANESPLIT) {
-    if (!lanesplit_supported(v.rate_lanes, msg_len, digest_bytes) || !args.aligned8) {
+    if (!whole_bytes || !lanesplit_supported(v.rate_lanes, msg_len, digest_bytes) || !args.aligned8) {
       set_error_text("lane-split kernel does not fit this batch");
       return B200SHA3_ERR_UNSUPPORTED;
     }

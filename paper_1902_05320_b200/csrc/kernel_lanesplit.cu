@@ -114,7 +114,7 @@ bool lanesplit_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes
 cudaError_t launch_hash_lanesplit(const HashArgs& args, const LaunchPlan& plan,
                                   cudaStream_t stream) {
   if (!lanesplit_supported(plan.rate_lanes, args.fixed_len, args.digest_bytes) || args.offsets ||
-      args.lengths || args.order || !args.aligned8) {
+      args.lengths || args.order || !args.aligned8 || args.last_mask != 0xffu) {
     return cudaErrorNotSupported;
   }
   const uint64_t per_block = static_cast<uint64_t>(kWarpsPerBlock) * kGroupsPerWarp;

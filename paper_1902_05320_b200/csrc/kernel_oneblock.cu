@@ -42,7 +42,7 @@ bool oneblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes)
 cudaError_t launch_hash_oneblock(const HashArgs& args, const LaunchPlan& plan,
                                  cudaStream_t stream) {
   if (!oneblock_supported(plan.rate_lanes, args.fixed_len, args.digest_bytes) ||
-      args.offsets || args.lengths || args.order || !args.aligned8) {
+      args.offsets || args.lengths || args.order || !args.aligned8 || args.last_mask != 0xffu) {
     return cudaErrorNotSupported;
   }
   const int ml = static_cast<int>(args.fixed_len / 8), ow = static_cast<int>(args.digest_bytes / 4);

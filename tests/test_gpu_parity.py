@@ -221,6 +221,33 @@ def test_oneblock_shapes(oracle, algorithm, msg_len, bits):
         Engine(kernel=KERNEL_ONEBLOCK).hash_fixed(algorithm, dev[:count * 24].contiguous(), 24, count, bits)
 
 
+@pytest.mark.parametrize("algorithm", [4, 5])
+@pytest.mark.parametrize("msg_len", [32, 64, 128])
+@pytest.mark.parametrize("bits", [250, 255, 509, 1023])
+def test_odd_bit_xof_on_oneblock_shapes(engine, oracle, algorithm, msg_len, bits):
+    """XOF lengths that are not whole bytes but round up to a one-block digest size (32 / 64 /
+    128 bytes): the last byte must come back masked (batch.cpp:22-24) through the device entry,
+    the host entry, and the forced one-block / lane-split kernels must refuse the batch rather
+    than return an unmasked byte."""
+    import torch
+    from paper_1902_05320_b200 import Engine, EngineError
+    from paper_1902_05320_b200.engine import KERNEL_LANESPLIT, KERNEL_ONEBLOCK
+    count = 1031
+    host = oracle.generate_workload(count * msg_len, msg_len, seed=77)
+    expect = oracle.hash_batch(algorithm, host, fixed_len=msg_len, count=count, xof_bits=bits)
+    assert all(oracle.hash_one(algorithm, host[i * msg_len:(i + 1) * msg_len].tobytes(), bits)
+               == expect[i].tobytes() for i in (0, 1, count - 1))
+    mask = (1 << (bits % 8)) - 1
+    assert (expect[:, -1] & ~np.uint8(mask) == 0).all() and (expect[:, -1] != 0).any()
+    dev = torch.from_numpy(host).cuda()
+    got = engine.hash_fixed(algorithm, dev, msg_len, count, bits)
+    assert (got.cpu().numpy() == expect).all()
+    assert (engine.hash_fixed(algorithm, host, msg_len, count, bits) == expect).all()
+    for forced in (KERNEL_ONEBLOCK, KERNEL_LANESPLIT):
+        with pytest.raises(EngineError):
+            Engine(kernel=forced).hash_fixed(algorithm, dev, msg_len, count, bits)
+
+
 @pytest.mark.parametrize("algorithm,msg_len,bits", [(1, 64, 0), (1, 8, 0), (1, 128, 0), (3, 64, 0),
                                                     (2, 96, 0), (5, 64, 512), (4, 160, 1344)])
 def test_lanesplit_kernel(oracle, algorithm, msg_len, bits):
