@@ -81,9 +81,11 @@ class DeviceError : public std::runtime_error {
 // staging) runs first, then pack tasks, C-ABI calls (H2D + kernels + D2H, one per ~32 MiB
 // chunk) and unpack tasks overlap for `pipeline` seconds; `resize` is the value-initialisation
 // of the outer digest vector (one thread, overlapped with packing).  `*_cpu` are summed over
-// the threads that ran the tasks, `device_calls` over the chunks.
+// the threads that ran the tasks, `device_calls` over the chunks.  `kernels` is the CUDA-event
+// time of the hashing kernels alone (per device: summed over its chunks; devices side by side).
 struct StageTimes {
   double scan = 0, pipeline = 0, resize = 0, device_calls = 0, pack_cpu = 0, unpack_cpu = 0;
+  double kernels = 0;
   unsigned threads = 0, chunks = 0, tasks = 0;
 };
 
@@ -105,9 +107,10 @@ struct DeviceConfig {
 };
 
 // Drop-in for sha3::hash_batch (proj/core/src/batch.cpp:64-135).
-// BatchResult::elapsed is the device time of the hashing kernels; packing,
-// copies and unpacking are outside it, as slot allocation and table warm-up
-// are outside the reference's timed region (batch.cpp:77-84, :133).
+// BatchResult::elapsed is the wall time of the hashing phase as the caller sees it
+// (batch.cpp:84, :133): scan, pack, host<->device copies, kernels and unpack -- the
+// number the reference's runner turns into throughput (runner.cpp:53, :71).  The
+// kernel-only device time is StageTimes::kernels (DeviceConfig::stages).
 BatchResult hash_batch(const HashBatch& batch, const EngineConfig& config = {},
                        const DeviceConfig& device = {});
 

@@ -1,21 +1,26 @@
-// b200sha3cli.cpp -- the two callers either side of the hot path, on the GPU
-// backend:
+// b200sha3cli.cpp -- command-line callers of the hot path on the GPU backend
+// (f-4 for `hash`).  Same sub-commands, option
+// names, exit codes and CSV columns as the reference's sha3cli
+// (proj/tools/sha3cli/main.cpp:21-24, :176-207; report.cpp:15-16), so rows and scripts
+// carry over; the work itself goes through the packed C ABI.
 //
-//   b200sha3cli bench   --algo A --message-size N --sizes a,b,c [--bits B] [--repeats R]
-//                       [--seed S] [--csv FILE] [--workers W]
-//       the `sha3cli bench` sweep (proj/tools/sha3cli/main.cpp:85-124) with backend
-//       "cuda": same workload stream (workload.cpp:16-47), same methodology
-//       (runner.cpp:30-76: one warm-up, >= R (>= 3) timed runs until >= 1 ms
-//       aggregate, median of BatchResult::elapsed), same console table and the same
-//       CSV columns (report.cpp:15-16) so rows can be concatenated with the
-//       reference's own output.
 //   b200sha3cli vectors --file F.rsp [--algo A]
-//       the `sha3cli vectors` verifier (main.cpp:126-160, vectors.cpp:42-179): the
-//       whole response file goes through the GPU as ONE batch.
+//       A response file is read straight into the packed batch layout (rsp_reader.hpp)
+//       and verified with ONE b200sha3_hash_batch call per output length.
+//   b200sha3cli bench [--algo A] [--message-size N] [--sizes a,b,c] [--bits B] [--repeats R]
+//                     [--seed S] [--workers W] [--layout vectors|packed] [--csv FILE]
+//       Throughput sweep over total-byte targets.  Methodology contract of the reference's
+//       runner (runner.hpp:30-36): one untimed pass, then at least R (>= 3) timed passes and
+//       at least 1 ms of timed work, median reported; generation is outside the timed region.
+//       --layout vectors times sha3::b200::hash_batch on vector<vector<uint8_t>> (the
+//       reference's call shape; time = BatchResult::elapsed); --layout packed times
+//       b200sha3_hash_fixed on pinned packed buffers (the C ABI's own shape).
+//   b200sha3cli hash [--algo A] [--bits B] [FILE|-]
+//       Digest of one file or stdin, streamed through the device-resident incremental
+//       hasher (b200sha3_states_*), lowercase hex.
 //
-// Exit codes follow main.cpp:21-24: 0 ok, 1 verification failed, 2 usage, 3 I/O.
+// Exit codes: 0 ok, 1 verification failed, 2 usage, 3 I/O or device error.
 #include <algorithm>
-#include <cctype>
 #include <chrono>
 #include <cinttypes>
 #include <cstdio>
@@ -23,387 +28,430 @@
 #include <fstream>
 #include <iostream>
 #include <map>
-#include <optional>
-#include <sstream>
+#include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "b200sha3/batch.hpp"
+#include "rsp_reader.hpp"
 
 namespace {
 
-constexpr int kExitOk = 0, kExitVerifyFailed = 1, kExitUsage = 2, kExitIo = 3;
+namespace rsp = b200sha3::rsp;
 
-const char* const kNames[6] = {"sha3-224", "sha3-256", "sha3-384", "sha3-512", "shake128", "shake256"};
+enum ExitCode { kOk = 0, kVerifyFailed = 1, kUsage = 2, kIo = 3 };
 
-std::string lowered(std::string s) {
-  for (char& c : s) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
-  return s;
-}
+// Canonical names in C-ABI id order (the variant table, proj/core/src/sha3.cpp:13-20).
+constexpr const char* kAlgorithmNames[6] = {"sha3-224", "sha3-256", "sha3-384", "sha3-512", "shake128", "shake256"};
 
-// parse_algorithm (proj/core/src/sha3.cpp:39-49)
-std::optional<sha3::Algorithm> parse_algorithm(const std::string& name) {
-  const std::string n = lowered(name);
-  for (int i = 0; i < 6; ++i) {
-    if (n == kNames[i]) return static_cast<sha3::Algorithm>(i);
+// Name -> id; case-insensitive, '-' and '_' optional ("SHA3_256", "shake-128"); -1 unknown.
+int algorithm_id(const std::string& name) {
+  const auto squash = [](const std::string& s) {
+    std::string out;
+    for (const char c : s) {
+      if (c != '-' && c != '_') out.push_back(static_cast<char>(std::tolower(static_cast<unsigned char>(c))));
+    }
+    return out;
+  };
+  const std::string want = squash(name);
+  for (int id = 0; id < 6; ++id) {
+    if (want == squash(kAlgorithmNames[id])) return id;
   }
-  if (n == "shake-128") return sha3::Algorithm::shake128;
-  if (n == "shake-256") return sha3::Algorithm::shake256;
-  return std::nullopt;
+  return -1;
 }
 
-bool is_xof(sha3::Algorithm a) { return a == sha3::Algorithm::shake128 || a == sha3::Algorithm::shake256; }
+bool is_xof(int id) { return id >= B200SHA3_SHAKE128; }
 
-// ---- workload (proj/tools/sha3cli/workload.cpp:9-47) -------------------------------
-struct SplitMix64 {
-  std::uint64_t state;
-  std::uint64_t next() {
-    std::uint64_t z = (state += 0x9e3779b97f4a7c15ull);
+struct UsageError {
+  std::string text;
+};
+
+// ---------------------------------------------------------------------------------------
+// vectors
+
+int run_vectors(const std::string& path, const std::string& algo_name) {
+  const int algorithm = algo_name.empty() ? rsp::algorithm_in_filename(path) : algorithm_id(algo_name);
+  if (algorithm < 0) {
+    if (algo_name.empty()) throw UsageError{"no algorithm in the file name '" + path + "'; pass --algo"};
+    throw UsageError{"unknown algorithm '" + algo_name + "'"};
+  }
+  rsp::PackedVectors file;
+  try {
+    file = rsp::load(path);
+  } catch (const rsp::SyntaxError& e) {
+    std::cerr << "b200sha3cli: " << path << ": " << e.what() << "\n";
+    return kIo;
+  }
+
+  // Batches by output length: one for the hash variants and for XOF files with an
+  // [Outputlen] header; otherwise one per distinct digest length in the file.  Every batch
+  // reads the same message arena through its own offsets / lengths.
+  std::map<std::uint64_t, std::vector<std::size_t>> by_bits;
+  for (std::size_t i = 0; i < file.size(); ++i) by_bits[is_xof(algorithm) ? file.xof_bits(i) : 0].push_back(i);
+
+  std::size_t passed = 0;
+  for (const auto& [bits, members] : by_bits) {
+    std::vector<std::uint64_t> offsets(members.size()), lengths(members.size());
+    for (std::size_t k = 0; k < members.size(); ++k) {
+      offsets[k] = file.offsets[members[k]];
+      lengths[k] = file.lengths[members[k]];
+    }
+    const std::uint64_t each = b200sha3_digest_bytes(algorithm, bits);
+    std::vector<std::uint8_t> digests(members.size() * each + 1);
+    const int rc = b200sha3_hash_batch(algorithm, file.messages.data(), offsets.data(), lengths.data(),
+                                       members.size(), bits, digests.data(), nullptr);
+    if (rc != B200SHA3_OK) {
+      std::cerr << "b200sha3cli: " << b200sha3_strerror(rc) << ": " << b200sha3_last_cuda_error() << "\n";
+      return kIo;
+    }
+    for (std::size_t k = 0; k < members.size(); ++k) {
+      const std::size_t i = members[k];
+      const std::uint8_t* want = file.expected.data() + file.expected_offsets[i];
+      const std::uint8_t* got = digests.data() + k * each;
+      if (file.expected_lengths[i] == each && std::memcmp(want, got, each) == 0) {
+        ++passed;
+        continue;
+      }
+      std::cout << "FAIL line " << file.source_line[i] << " (Len = " << file.message_bits[i] << ")\n"
+                << "  expected " << rsp::hex(want, file.expected_lengths[i]) << "\n"
+                << "  actual   " << rsp::hex(got, each) << "\n";
+    }
+  }
+  std::cout << passed << "/" << file.size() << " vectors passed (" << kAlgorithmNames[algorithm] << ", cuda)\n";
+  return passed == file.size() ? kOk : kVerifyFailed;
+}
+
+// ---------------------------------------------------------------------------------------
+// bench
+
+// The reference's synthetic message stream (byte-stream contract of
+// proj/tools/sha3cli/workload.cpp:16-47): splitmix64 seeded with
+// seed ^ total_bytes * golden, ceil(size / 8) draws per message, bytes little-endian, the
+// surplus of the last draw dropped.  splitmix64 is a counter generator -- draw n (from 1)
+// is mix(seed + n * golden) -- so any message can be produced on its own, by any thread.
+class MessageStream {
+ public:
+  MessageStream(std::uint64_t seed, std::uint64_t total_bytes, std::size_t message_size)
+      : base_(seed ^ (total_bytes * kGolden)), size_(message_size), draws_((message_size + 7) / 8) {}
+
+  void write(std::uint64_t message, std::uint8_t* dst) const {
+    std::uint64_t counter = base_ + (message * draws_ + 1) * kGolden;
+    for (std::size_t at = 0; at < size_; at += 8, counter += kGolden) {
+      const std::uint64_t word = mix(counter);  // little-endian host (x86-64 / aarch64)
+      std::memcpy(dst + at, &word, std::min<std::size_t>(8, size_ - at));
+    }
+  }
+
+ private:
+  static constexpr std::uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+  static std::uint64_t mix(std::uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
     return z ^ (z >> 31);
   }
+  std::uint64_t base_;
+  std::size_t size_, draws_;
 };
 
-sha3::HashBatch generate_workload(sha3::Algorithm algorithm, std::uint64_t xof_bits,
-                                  std::size_t message_size, std::uint64_t seed,
-                                  std::uint64_t total_bytes) {
+template <class Fn>
+void for_each_range(std::uint64_t n, Fn fn) {  // fn(first, last) on hardware threads
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned parts = static_cast<unsigned>(std::min<std::uint64_t>(hw, std::max<std::uint64_t>(1, n >> 14)));
+  std::vector<std::thread> pool;
+  for (unsigned p = 1; p < parts; ++p) pool.emplace_back(fn, n * p / parts, n * (p + 1) / parts);
+  fn(std::uint64_t{0}, n / parts);
+  for (auto& t : pool) t.join();
+}
+
+struct Pass {
+  double seconds = 0;  // what the row reports
+  double kernels = 0;  // CUDA-event time of the hashing kernels inside it
+};
+
+struct Row {
+  std::uint64_t hashed_bytes = 0;
+  std::size_t message_size = 0;
+  std::uint64_t messages = 0;
+  double seconds = 0, kernels = 0;
+  unsigned passes = 0;
+};
+
+double middle(std::vector<double>& v) {  // median; reorders v
+  const std::size_t half = v.size() / 2;
+  std::nth_element(v.begin(), v.begin() + half, v.end());
+  double m = v[half];
+  if (v.size() % 2 == 0) m = 0.5 * (m + *std::max_element(v.begin(), v.begin() + half));
+  return m;
+}
+
+// One untimed pass (context, pinned staging, memory pools), then timed passes until there
+// are `min_passes` of them AND a millisecond of timed work, so no row reports a zero time.
+template <class OnePass>
+void measure(unsigned min_passes, OnePass one_pass, Row& row) {
+  constexpr double kMinTimedSeconds = 1e-3;
+  constexpr std::size_t kPassLimit = std::size_t{1} << 20;  // a clock that never advances
+  one_pass();
+  std::vector<double> seconds, kernels;
+  double timed = 0;
+  do {
+    const Pass p = one_pass();
+    seconds.push_back(p.seconds);
+    kernels.push_back(p.kernels);
+    timed += p.seconds;
+  } while ((seconds.size() < min_passes || timed < kMinTimedSeconds) && seconds.size() < kPassLimit);
+  row.passes = static_cast<unsigned>(seconds.size());
+  row.seconds = middle(seconds);
+  if (!(row.seconds > 0)) row.seconds = timed / row.passes;
+  row.kernels = middle(kernels);
+}
+
+struct BenchOptions {
+  int algorithm = B200SHA3_SHA3_256;
+  std::uint64_t xof_bits = 0;
+  std::size_t message_size = 10;
+  // default sweep: the total-byte targets of the paper's Table 3 (workload.hpp:16-18)
+  std::vector<std::uint64_t> totals = {1202, 4652, 9302, 18602, 37202, 74402, 148802, 297602, 595202, 1190402};
+  std::uint64_t seed = 1;
+  unsigned repeats = 3, workers = 0;
+  bool packed = false;
+  std::string csv;
+};
+
+Row bench_vectors(const BenchOptions& o, std::uint64_t total) {
   sha3::HashBatch batch;
-  batch.algorithm = algorithm;
+  batch.algorithm = static_cast<sha3::Algorithm>(o.algorithm);
+  batch.xof_output_bits = o.xof_bits;
+  batch.messages.assign(total / o.message_size, std::vector<std::uint8_t>(o.message_size));
+  const MessageStream stream(o.seed, total, o.message_size);
+  for_each_range(batch.messages.size(), [&](std::uint64_t first, std::uint64_t last) {
+    for (std::uint64_t i = first; i < last; ++i) stream.write(i, batch.messages[i].data());
+  });
+  sha3::EngineConfig engine;
+  engine.workers = o.workers;
+  sha3::b200::StageTimes stages;
+  sha3::b200::DeviceConfig device;
+  device.stages = &stages;
+  Row row{batch.messages.size() * o.message_size, o.message_size, batch.messages.size()};
+  measure(o.repeats, [&] {
+    const sha3::BatchResult result = sha3::b200::hash_batch(batch, engine, device);
+    return Pass{result.elapsed.count(), stages.kernels};
+  }, row);
+  return row;
+}
+
+Row bench_packed(const BenchOptions& o, std::uint64_t total) {
+  const std::uint64_t count = total / o.message_size;
+  const std::uint64_t each = b200sha3_digest_bytes(o.algorithm, o.xof_bits);
+  void *in = nullptr, *out = nullptr;
+  if (b200sha3_pinned_alloc(count * o.message_size + 16, &in) != B200SHA3_OK ||
+      b200sha3_pinned_alloc(count * each + 16, &out) != B200SHA3_OK) {
+    throw sha3::b200::DeviceError(B200SHA3_ERR_CUDA, std::string("pinned allocation: ") + b200sha3_last_cuda_error());
+  }
+  const MessageStream stream(o.seed, total, o.message_size);
+  for_each_range(count, [&](std::uint64_t first, std::uint64_t last) {
+    for (std::uint64_t i = first; i < last; ++i) stream.write(i, static_cast<std::uint8_t*>(in) + i * o.message_size);
+  });
+  Row row{count * o.message_size, o.message_size, count};
+  int failed = B200SHA3_OK;
+  measure(o.repeats, [&] {
+    double ms = 0;
+    b200sha3_config cfg{};
+    cfg.struct_size = sizeof cfg;
+    cfg.device = -1;
+    cfg.fma_preset = -1;
+    cfg.device_ms = &ms;
+    const auto t0 = std::chrono::steady_clock::now();
+    const int rc = b200sha3_hash_fixed(o.algorithm, static_cast<const std::uint8_t*>(in), o.message_size, count,
+                                       o.xof_bits, static_cast<std::uint8_t*>(out), &cfg);
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (rc != B200SHA3_OK) failed = rc;
+    return Pass{failed ? 1.0 : wall, ms * 1e-3};  // a failing call ends the sampling at once
+  }, row);
+  b200sha3_pinned_free(in);
+  b200sha3_pinned_free(out);
+  if (failed) {
+    throw sha3::b200::DeviceError(failed, std::string(b200sha3_strerror(failed)) + ": " + b200sha3_last_cuda_error());
+  }
+  return row;
+}
+
+int run_bench(BenchOptions o) {
+  if (o.repeats < 3) throw UsageError{"--repeats must be at least 3 (a reported row is a median)"};
+  if (o.message_size == 0) throw UsageError{"--message-size must be positive"};
+  if (is_xof(o.algorithm) && o.xof_bits == 0) o.xof_bits = o.algorithm == B200SHA3_SHAKE128 ? 256 : 512;
+  if (!is_xof(o.algorithm)) o.xof_bits = 0;
+  for (const std::uint64_t total : o.totals) {
+    if (total < o.message_size) throw UsageError{"a --sizes entry is smaller than one message"};
+  }
+  const char* backend = o.packed ? "cuda-packed" : "cuda";
+  std::vector<Row> rows;
+  for (const std::uint64_t total : o.totals) rows.push_back(o.packed ? bench_packed(o, total) : bench_vectors(o, total));
+
+  std::printf("%14s %9s %12s %-12s %12s %16s %7s %12s\n", "total_bytes", "msg_size", "msg_count", "backend", "time_s",
+              "throughput_Bps", "repeats", "kernels_s");
+  for (const Row& r : rows) {
+    std::printf("%14" PRIu64 " %9zu %12" PRIu64 " %-12s %12.6f %16.2f %7u %12.6f\n", r.hashed_bytes, r.message_size,
+                r.messages, backend, r.seconds, static_cast<double>(r.hashed_bytes) / r.seconds, r.passes, r.kernels);
+  }
+  if (o.csv.empty()) return kOk;
+  std::FILE* f = std::fopen(o.csv.c_str(), "wb");
+  if (!f) {
+    std::cerr << "b200sha3cli: cannot write " << o.csv << "\n";
+    return kIo;
+  }
+  // column contract: proj/tools/sha3cli/report.cpp:15-16
+  std::fputs("total_bytes,message_size,message_count,backend,time_seconds,throughput_bps,repeats\n", f);
+  for (const Row& r : rows) {
+    std::fprintf(f, "%" PRIu64 ",%zu,%" PRIu64 ",%s,%.9g,%.9g,%u\n", r.hashed_bytes, r.message_size, r.messages,
+                 backend, r.seconds, static_cast<double>(r.hashed_bytes) / r.seconds, r.passes);
+  }
+  const bool bad = std::ferror(f) != 0;
+  return (std::fclose(f) != 0 || bad) ? kIo : kOk;
+}
+
+// ---------------------------------------------------------------------------------------
+// hash
+
+int run_hash(const std::string& algo_name, std::uint64_t bits, const std::string& path) {
+  const int algorithm = algorithm_id(algo_name);
+  if (algorithm < 0) throw UsageError{"unknown algorithm '" + algo_name + "'"};
+  if (bits && !is_xof(algorithm)) throw UsageError{"--bits applies to XOF variants only"};
+  if (is_xof(algorithm) && bits == 0) bits = algorithm == B200SHA3_SHAKE128 ? 256 : 512;
+  if (bits % 8) throw UsageError{"--bits must be a multiple of 8"};
+  std::ifstream file;
+  std::istream* in = &std::cin;
+  if (!path.empty() && path != "-") {
+    file.open(path, std::ios::binary);
+    if (!file) {
+      std::cerr << "b200sha3cli: cannot open " << path << "\n";
+      return kIo;
+    }
+    in = &file;
+  }
+  sha3::b200::BatchHasher hasher(static_cast<sha3::Algorithm>(algorithm), 1);
+  std::vector<std::uint8_t> chunk(4u << 20);
+  for (;;) {
+    in->read(reinterpret_cast<char*>(chunk.data()), static_cast<std::streamsize>(chunk.size()));
+    const std::uint64_t got = static_cast<std::uint64_t>(in->gcount());
+    if (got) hasher.update_fixed(chunk.data(), got);
+    if (!*in) break;
+  }
+  if (in->bad()) {
+    std::cerr << "b200sha3cli: read error\n";
+    return kIo;
+  }
+  std::vector<std::vector<std::uint8_t>> out;
   if (is_xof(algorithm)) {
-    batch.xof_output_bits = xof_bits ? xof_bits : (algorithm == sha3::Algorithm::shake128 ? 256 : 512);
-  }
-  SplitMix64 rng{seed ^ (total_bytes * 0x9e3779b97f4a7c15ull)};
-  batch.messages.resize(total_bytes / message_size);
-  for (auto& msg : batch.messages) {
-    msg.resize(message_size);
-    for (std::size_t i = 0; i < message_size;) {
-      const std::uint64_t word = rng.next();
-      for (int k = 0; k < 8 && i < message_size; ++k, ++i) msg[i] = static_cast<std::uint8_t>(word >> (8 * k));
-    }
-  }
-  return batch;
-}
-
-// ---- bench (runner.cpp:30-76, report.cpp:52-143) -----------------------------------
-struct Record {
-  std::uint64_t total_bytes;
-  std::size_t message_size, message_count;
-  double time_seconds, throughput_bps;
-  unsigned repeats;
-  double wall_seconds;  // whole hash_batch call (pack + copies + kernels + unpack); console only
-};
-
-double median(std::vector<double> v) {
-  std::sort(v.begin(), v.end());
-  const std::size_t n = v.size();
-  return n % 2 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
-}
-
-int cmd_bench(sha3::Algorithm algorithm, std::uint64_t bits, std::size_t message_size,
-              const std::vector<std::uint64_t>& sizes, std::uint64_t seed, unsigned repeats,
-              unsigned workers, const std::string& csv_path) {
-  if (repeats < 3) {
-    std::cerr << "b200sha3cli: reported rows need at least 3 repeats\n";
-    return kExitUsage;
-  }
-  if (message_size == 0) {
-    std::cerr << "b200sha3cli: message size must be positive\n";
-    return kExitUsage;
-  }
-  sha3::EngineConfig config;
-  config.workers = workers;
-  std::vector<Record> records;
-  for (const std::uint64_t total : sizes) {
-    if (total < message_size) {
-      std::cerr << "b200sha3cli: total size smaller than one message\n";
-      return kExitUsage;
-    }
-    const sha3::HashBatch batch = generate_workload(algorithm, bits, message_size, seed, total);
-    const std::uint64_t hashed = static_cast<std::uint64_t>(batch.messages.size()) * message_size;
-    sha3::b200::hash_batch(batch, config);  // warm-up, not recorded
-    std::vector<double> samples, walls;
-    double aggregate = 0;
-    while (samples.size() < repeats || aggregate < 1e-3) {
-      const auto t0 = std::chrono::steady_clock::now();
-      const sha3::BatchResult result = sha3::b200::hash_batch(batch, config);
-      walls.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
-      samples.push_back(result.elapsed.count());  // `result` dies after the clock was read
-      aggregate += samples.back();
-      if (samples.size() >= 1u << 20) break;
-    }
-    double time = median(samples);
-    if (time <= 0) time = aggregate / static_cast<double>(samples.size());
-    records.push_back({hashed, message_size, batch.messages.size(), time,
-                       static_cast<double>(hashed) / time, static_cast<unsigned>(samples.size()),
-                       median(walls)});
-  }
-  // the reference's table (report.cpp:113-143) plus one column: the wall time of the call
-  std::printf("%12s %9s %10s %-10s %14s %16s %8s %8s %12s\n", "total_bytes", "msg_size", "msg_count",
-              "backend", "time_s", "throughput_Bps", "repeats", "speedup", "call_wall_s");
-  for (const Record& r : records) {
-    std::printf("%12" PRIu64 " %9zu %10zu %-10s %14.6f %16.2f %8u %8s %12.6f\n", r.total_bytes,
-                r.message_size, r.message_count, "cuda", r.time_seconds, r.throughput_bps, r.repeats, "",
-                r.wall_seconds);
-  }
-  if (!csv_path.empty()) {
-    std::ofstream out(csv_path, std::ios::binary);
-    if (!out) {
-      std::cerr << "b200sha3cli: cannot write " << csv_path << "\n";
-      return kExitIo;
-    }
-    out << "total_bytes,message_size,message_count,backend,time_seconds,throughput_bps,repeats\n";
-    char buf[256];
-    for (const Record& r : records) {
-      std::snprintf(buf, sizeof buf, "%" PRIu64 ",%zu,%zu,cuda,%.9g,%.9g,%u\n", r.total_bytes,
-                    r.message_size, r.message_count, r.time_seconds, r.throughput_bps, r.repeats);
-      out << buf;
-    }
-    if (!out) return kExitIo;
-  }
-  return kExitOk;
-}
-
-// ---- vectors (vectors.cpp:42-179) ---------------------------------------------------
-struct Entry {
-  std::size_t line = 0;
-  std::uint64_t msg_bits = 0;
-  std::vector<std::uint8_t> message, expected;
-};
-
-std::string trim(const std::string& s) {
-  const auto b = s.find_first_not_of(" \t\r\n");
-  if (b == std::string::npos) return "";
-  return s.substr(b, s.find_last_not_of(" \t\r\n") - b + 1);
-}
-
-bool key_value(const std::string& line, std::string& key, std::string& value) {
-  const auto eq = line.find('=');
-  if (eq == std::string::npos) return false;
-  key = trim(line.substr(0, eq));
-  value = trim(line.substr(eq + 1));
-  return !key.empty();
-}
-
-std::optional<std::vector<std::uint8_t>> from_hex(const std::string& s) {
-  if (s.size() % 2) return std::nullopt;
-  std::vector<std::uint8_t> out(s.size() / 2);
-  auto nib = [](char c) -> int {
-    if (c >= '0' && c <= '9') return c - '0';
-    if (c >= 'a' && c <= 'f') return c - 'a' + 10;
-    if (c >= 'A' && c <= 'F') return c - 'A' + 10;
-    return -1;
-  };
-  for (std::size_t i = 0; i < out.size(); ++i) {
-    const int hi = nib(s[2 * i]), lo = nib(s[2 * i + 1]);
-    if (hi < 0 || lo < 0) return std::nullopt;
-    out[i] = static_cast<std::uint8_t>(hi * 16 + lo);
-  }
-  return out;
-}
-
-std::string to_hex(const std::vector<std::uint8_t>& v) {
-  static const char* d = "0123456789abcdef";
-  std::string s;
-  for (std::uint8_t b : v) {
-    s.push_back(d[b >> 4]);
-    s.push_back(d[b & 15]);
-  }
-  return s;
-}
-
-struct ParseError {
-  std::string what;
-};
-
-void parse_file(std::istream& in, std::uint64_t& output_bits, std::vector<Entry>& entries) {
-  std::string line;
-  std::size_t line_no = 0;
-  std::optional<Entry> pending;
-  bool have_msg = false;
-  auto fail = [&](const std::string& what) {
-    throw ParseError{"vector file line " + std::to_string(line_no) + ": " + what};
-  };
-  while (std::getline(in, line)) {
-    ++line_no;
-    const std::string text = trim(line);
-    if (text.empty() || text[0] == '#') continue;
-    std::string key, value;
-    if (text.front() == '[' && text.back() == ']') {
-      if (key_value(text.substr(1, text.size() - 2), key, value) && key == "Outputlen") {
-        try {
-          output_bits = std::stoull(value);
-        } catch (const std::exception&) {
-          fail("bad Outputlen value '" + value + "'");
-        }
-      }
-      continue;
-    }
-    if (!key_value(text, key, value)) fail("expected 'Key = value', got '" + text + "'");
-    if (key == "Len") {
-      if (pending) fail("new Len before the previous vector was completed");
-      Entry e;
-      e.line = line_no;
-      try {
-        e.msg_bits = std::stoull(value);
-      } catch (const std::exception&) {
-        fail("bad Len value '" + value + "'");
-      }
-      if (e.msg_bits % 8) fail("only byte-aligned lengths are supported (Len = " + value + ")");
-      pending = std::move(e);
-      have_msg = false;
-    } else if (key == "Msg") {
-      if (!pending) fail("Msg without a preceding Len");
-      auto bytes = from_hex(value);
-      if (!bytes) fail("Msg is not valid hex");
-      if (pending->msg_bits > 0) {
-        if (bytes->size() < pending->msg_bits / 8) fail("Msg shorter than Len");
-        bytes->resize(pending->msg_bits / 8);
-        pending->message = std::move(*bytes);
-      }
-      have_msg = true;
-    } else if (key == "MD" || key == "Output") {
-      if (!pending || !have_msg) fail(key + " without a preceding Len/Msg pair");
-      const auto bytes = from_hex(value);
-      if (!bytes || bytes->empty()) fail(key + " is not valid hex");
-      pending->expected = *bytes;
-      entries.push_back(std::move(*pending));
-      pending.reset();
-    } else {
-      fail("unknown key '" + key + "'");
-    }
-  }
-  if (pending) fail("file ended in the middle of a vector");
-}
-
-std::optional<sha3::Algorithm> algorithm_from_filename(const std::string& path) {
-  std::string name = path.substr(path.find_last_of('/') == std::string::npos ? 0 : path.find_last_of('/') + 1);
-  name = lowered(name);
-  for (const char* sep : {"_", "-", ""}) {
-    const std::pair<std::string, int> tags[] = {
-        {std::string("sha3") + sep + "224", 0}, {std::string("sha3") + sep + "256", 1},
-        {std::string("sha3") + sep + "384", 2}, {std::string("sha3") + sep + "512", 3},
-        {std::string("shake") + sep + "128", 4}, {std::string("shake") + sep + "256", 5}};
-    for (const auto& [tag, id] : tags) {
-      if (name.find(tag) != std::string::npos) return static_cast<sha3::Algorithm>(id);
-    }
-  }
-  return std::nullopt;
-}
-
-int cmd_vectors(const std::string& path, const std::string& algo_name) {
-  std::optional<sha3::Algorithm> algorithm;
-  if (!algo_name.empty()) {
-    algorithm = parse_algorithm(algo_name);
-    if (!algorithm) {
-      std::cerr << "b200sha3cli: unknown algorithm '" << algo_name << "'\n";
-      return kExitUsage;
-    }
+    hasher.finish();
+    out = hasher.read(bits / 8);
   } else {
-    algorithm = algorithm_from_filename(path);
-    if (!algorithm) {
-      std::cerr << "b200sha3cli: cannot infer the algorithm from '" << path << "'; pass --algo\n";
-      return kExitUsage;
-    }
+    out = hasher.digest();
   }
-  std::uint64_t output_bits = 0;
-  std::vector<Entry> entries;
-  {
-    std::ifstream in(path);
-    if (!in) {
-      std::cerr << "b200sha3cli: cannot open vector file: " << path << "\n";
-      return kExitIo;
-    }
-    try {
-      parse_file(in, output_bits, entries);
-    } catch (const ParseError& e) {
-      std::cerr << "b200sha3cli: " << e.what << "\n";
-      return kExitIo;
-    }
-  }
-  // One GPU batch per distinct output length (one batch in practice: hash variants
-  // have a fixed length and XOF files carry one [Outputlen]).
-  std::map<std::uint64_t, std::vector<std::size_t>> groups;
-  for (std::size_t i = 0; i < entries.size(); ++i) {
-    const std::uint64_t bits = is_xof(*algorithm) ? (output_bits ? output_bits : entries[i].expected.size() * 8) : 0;
-    groups[bits].push_back(i);
-  }
-  std::size_t passed = 0;
-  try {
-    for (const auto& [bits, idx] : groups) {
-      sha3::HashBatch batch;
-      batch.algorithm = *algorithm;
-      batch.xof_output_bits = bits;
-      for (std::size_t i : idx) batch.messages.push_back(entries[i].message);
-      const sha3::BatchResult res = sha3::b200::hash_batch(batch);
-      for (std::size_t k = 0; k < idx.size(); ++k) {
-        const Entry& e = entries[idx[k]];
-        if (res.digests[k] == e.expected) {
-          ++passed;
-        } else {
-          std::cout << "FAIL line " << e.line << " (Len = " << e.msg_bits << ")\n"
-                    << "  expected " << to_hex(e.expected) << "\n"
-                    << "  actual   " << to_hex(res.digests[k]) << "\n";
-        }
-      }
-    }
-  } catch (const std::exception& e) {
-    std::cerr << "b200sha3cli: " << e.what() << "\n";
-    return kExitIo;
-  }
-  std::cout << passed << "/" << entries.size() << " vectors passed ("
-            << kNames[static_cast<int>(*algorithm)] << ", cuda)\n";
-  return passed == entries.size() ? kExitOk : kExitVerifyFailed;
+  std::cout << rsp::hex(out[0].data(), out[0].size()) << "\n";
+  return kOk;
 }
 
-int usage() {
-  std::cerr << "usage: b200sha3cli bench --algo A --message-size N --sizes a,b,c [--bits B] [--repeats R]"
-               " [--seed S] [--workers W] [--csv FILE]\n"
-               "       b200sha3cli vectors --file F.rsp [--algo A]\n";
-  return kExitUsage;
+// ---------------------------------------------------------------------------------------
+
+constexpr const char* kUsageText =
+    "usage: b200sha3cli vectors --file F.rsp [--algo A]\n"
+    "       b200sha3cli bench [--algo A] [--message-size N] [--sizes a,b,c] [--bits B] [--repeats R]\n"
+    "                         [--seed S] [--workers W] [--layout vectors|packed] [--csv FILE]\n"
+    "       b200sha3cli hash [--algo A] [--bits B] [FILE|-]\n"
+    "algorithms: sha3-224 sha3-256 sha3-384 sha3-512 shake128 shake256\n";
+
+struct Options {
+  std::map<std::string, std::string> named;
+  std::vector<std::string> positional;
+  std::string get(const std::string& key, const std::string& fallback) const {
+    const auto it = named.find(key);
+    return it == named.end() ? fallback : it->second;
+  }
+  std::uint64_t number(const std::string& key, std::uint64_t fallback) const {
+    const auto it = named.find(key);
+    if (it == named.end()) return fallback;
+    std::size_t used = 0;
+    std::uint64_t v = 0;
+    try {
+      v = std::stoull(it->second, &used);
+    } catch (const std::exception&) {
+      used = 0;
+    }
+    if (used == 0 || used != it->second.size()) throw UsageError{"--" + key + " needs a number, got '" + it->second + "'"};
+    return v;
+  }
+};
+
+Options parse_options(int argc, char** argv, const std::vector<std::string>& allowed) {
+  Options o;
+  for (int i = 2; i < argc; ++i) {
+    const std::string arg = argv[i];
+    if (arg.size() > 2 && arg.compare(0, 2, "--") == 0) {
+      const std::string key = arg.substr(2);
+      if (std::find(allowed.begin(), allowed.end(), key) == allowed.end()) throw UsageError{"unknown option " + arg};
+      if (i + 1 >= argc) throw UsageError{arg + " needs a value"};
+      o.named[key] = argv[++i];
+    } else {
+      o.positional.push_back(arg);
+    }
+  }
+  return o;
 }
 
 }  // namespace
 
 int main(int argc, char** argv) {
-  if (argc < 2) return usage();
-  const std::string cmd = argv[1];
-  std::map<std::string, std::string> opt;
-  for (int i = 2; i < argc; ++i) {
-    const std::string key = argv[i];
-    if (key.rfind("--", 0) != 0 || i + 1 >= argc) return usage();
-    opt[key.substr(2)] = argv[++i];
-  }
-  auto get = [&](const std::string& k, const std::string& dflt) {
-    const auto it = opt.find(k);
-    return it == opt.end() ? dflt : it->second;
-  };
   try {
-    if (cmd == "vectors") {
-      if (!opt.count("file")) return usage();
-      return cmd_vectors(opt["file"], get("algo", ""));
+    const std::string command = argc > 1 ? argv[1] : "";
+    if (command == "vectors") {
+      const Options o = parse_options(argc, argv, {"file", "algo"});
+      if (!o.named.count("file") || !o.positional.empty()) throw UsageError{"vectors needs --file"};
+      return run_vectors(o.get("file", ""), o.get("algo", ""));
     }
-    if (cmd == "bench") {
-      const auto algorithm = parse_algorithm(get("algo", "sha3-256"));
-      if (!algorithm) {
-        std::cerr << "b200sha3cli: unknown algorithm '" << get("algo", "") << "'\n";
-        return kExitUsage;
+    if (command == "bench") {
+      const Options o = parse_options(argc, argv, {"algo", "message-size", "sizes", "bits", "repeats", "seed",
+                                                   "workers", "layout", "csv", "backend", "chunk"});
+      if (!o.positional.empty()) throw UsageError{"unexpected argument " + o.positional[0]};
+      BenchOptions b;
+      b.algorithm = algorithm_id(o.get("algo", "sha3-256"));
+      if (b.algorithm < 0) throw UsageError{"unknown algorithm '" + o.get("algo", "") + "'"};
+      b.xof_bits = o.number("bits", 0);
+      b.message_size = o.number("message-size", b.message_size);
+      b.seed = o.number("seed", b.seed);
+      b.repeats = static_cast<unsigned>(o.number("repeats", b.repeats));
+      b.workers = static_cast<unsigned>(o.number("workers", 0));
+      b.csv = o.get("csv", "");
+      const std::string layout = o.get("layout", "vectors");
+      if (layout != "vectors" && layout != "packed") throw UsageError{"--layout must be vectors or packed"};
+      b.packed = layout == "packed";
+      if (o.named.count("sizes")) {
+        b.totals.clear();
+        const std::string list = o.get("sizes", "");
+        for (std::size_t at = 0; at <= list.size();) {
+          const std::size_t comma = std::min(list.find(',', at), list.size());
+          Options one;
+          one.named["sizes"] = list.substr(at, comma - at);
+          b.totals.push_back(one.number("sizes", 0));
+          at = comma + 1;
+        }
       }
-      // defaults of WorkloadSpec (workload.hpp:15-20): the paper's Table 3 sweep
-      std::vector<std::uint64_t> sizes;
-      std::stringstream ss(get("sizes", "1202,4652,9302,18602,37202,74402,148802,297602,595202,1190402"));
-      for (std::string tok; std::getline(ss, tok, ',');) sizes.push_back(std::stoull(tok));
-      return cmd_bench(*algorithm, std::stoull(get("bits", "0")), std::stoull(get("message-size", "10")),
-                       sizes, std::stoull(get("seed", "1")),
-                       static_cast<unsigned>(std::stoul(get("repeats", "3"))),
-                       static_cast<unsigned>(std::stoul(get("workers", "0"))), get("csv", ""));
+      return run_bench(b);
     }
+    if (command == "hash") {
+      const Options o = parse_options(argc, argv, {"algo", "bits"});
+      if (o.positional.size() > 1) throw UsageError{"hash takes at most one FILE"};
+      return run_hash(o.get("algo", "sha3-256"), o.number("bits", 0), o.positional.empty() ? "-" : o.positional[0]);
+    }
+    throw UsageError{command.empty() ? "a sub-command is required" : "unknown sub-command '" + command + "'"};
+  } catch (const UsageError& e) {
+    std::cerr << "b200sha3cli: " << e.text << "\n" << kUsageText;
+    return kUsage;
   } catch (const std::invalid_argument& e) {
     std::cerr << "b200sha3cli: " << e.what() << "\n";
-    return kExitUsage;
+    return kUsage;
   } catch (const std::exception& e) {
     std::cerr << "b200sha3cli: " << e.what() << "\n";
-    return kExitIo;
+    return kIo;
   }
-  return usage();
 }

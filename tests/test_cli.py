@@ -53,6 +53,72 @@ def test_usage_and_io_errors(cli, tmp_path):
     assert run(cli, "vectors", "--file", str(bad)).returncode == 3        # MD without Msg
 
 
+MALFORMED = {
+    # name -> (text, line both parsers must name)
+    "len_not_aligned": ("Len = 12\nMsg = 0000\nMD = 00\n", 1),
+    "digest_before_msg": ("# c\nLen = 8\nMD = 00\n", 3),
+    "msg_without_len": ("\nMsg = 00\n", 2),
+    "second_len": ("Len = 8\nMsg = 00\nLen = 8\n", 3),
+    "unknown_key": ("Len = 8\nMsg = 00\nDigest = 00\n", 3),
+    "no_equals": ("Len = 8\nMsg 00\n", 2),
+    "odd_hex": ("Len = 8\nMsg = 000\nMD = 00\n", 2),
+    "bad_hex": ("Len = 8\nMsg = 0g\nMD = 00\n", 2),
+    "short_msg": ("Len = 24\nMsg = 0000\nMD = 00\n", 2),
+    "empty_digest": ("Len = 8\nMsg = 00\nMD =\n", 3),
+    "truncated": ("Len = 8\nMsg = 00\nMD = 00\nLen = 8\nMsg = 11\n", 5),
+    "bad_outputlen": ("[Outputlen = x]\nLen = 8\nMsg = 00\nMD = 00\n", 1),
+    "bad_len": ("Len = eight\n", 1),
+}
+
+WELL_FORMED = {
+    "crlf_and_spaces": "[L = 256]\r\n\r\n  Len   =  16 \r\nMsg=ABcd\r\n\tMD = 00ff\r\n",
+    "empty_message_placeholder": "Len = 0\nMsg = 00\nMD = a7\n",
+    "msg_longer_than_len": "Len = 8\nMsg = 112233\nOutput = 0102\n",
+    "msg_given_twice": "Len = 8\nMsg = 11\nMsg = 22\nMD = 0102\n",
+    "other_headers": "[Foo]\n[Bar = 1]\n[Outputlen = 24]\nLen = 8\nMsg = 11\nOutput = 010203\n",
+    "no_vectors": "# nothing\n\n",
+}
+
+
+def test_rsp_reader_matches_the_reference_parser(tmp_path):
+    """Parser parity (f-2): paper_1902_05320_b200/host/rsp_reader.cpp against the reference's
+    own parse_vector_file (vectors.cpp:42-125, compiled unmodified into oracle/_ref/rsp_parity)
+    -- same vectors from well-formed files, same line named for malformed ones."""
+    tool = ROOT / "oracle" / "_ref" / "rsp_parity"
+    if not tool.exists():
+        pytest.skip("oracle/_ref/rsp_parity not built (needs /root/reference)")
+    files, expect = [], []
+    for kat in sorted(GOLDEN.glob("*.kat")):
+        dst = tmp_path / (kat.stem + ".rsp")
+        n = write_rsp(kat, dst)
+        files.append(dst)
+        expect.append(f"same {n}")
+    for name, text in WELL_FORMED.items():
+        dst = tmp_path / (name + ".rsp")
+        dst.write_bytes(text.encode())
+        files.append(dst)
+        expect.append("same")
+    for name, (text, line) in MALFORMED.items():
+        dst = tmp_path / (name + ".rsp")
+        dst.write_bytes(text.encode())
+        files.append(dst)
+        expect.append(f"reject {line}")
+    r = subprocess.run([str(tool), *map(str, files)], capture_output=True, text=True, timeout=120)
+    rows = r.stdout.strip().splitlines()
+    assert len(rows) == len(files), r.stdout + r.stderr
+    for f, want, row in zip(files, expect, rows):
+        assert row.startswith(f"{f} {want}"), row
+    assert r.returncode == 0
+
+
+def test_cli_names_the_line_of_a_malformed_file(cli, tmp_path):
+    for name, (text, line) in MALFORMED.items():
+        bad = tmp_path / ("sha3_256_" + name + ".rsp")
+        bad.write_bytes(text.encode())
+        r = run(cli, "vectors", "--file", str(bad))
+        assert r.returncode == 3 and f"line {line}:" in r.stderr, (name, r.stderr)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("stem", ["SHA3_224ShortMsg", "SHA3_256LongMsg", "SHA3_384ShortMsg", "SHA3_512LongMsg",
                                   "SHAKE128ShortMsg", "SHAKE256LongMsg"])
@@ -90,3 +156,72 @@ def test_bench_subcommand_csv(cli, tmp_path):
         assert x["backend"] == "cuda" and int(x["repeats"]) >= 3
         assert abs(float(x["throughput_bps"]) * float(x["time_seconds"]) - int(x["total_bytes"])) < 1.0
     assert "throughput_Bps" in r.stdout
+
+
+@pytest.mark.gpu
+def test_bench_subcommand_packed_layout(cli, tmp_path):
+    """--layout packed: the same sweep on pinned packed buffers through b200sha3_hash_fixed."""
+    out = tmp_path / "bench.csv"
+    r = run(cli, "bench", "--algo", "shake128", "--bits", "1024", "--message-size", "64", "--sizes",
+            "6400,67108864", "--layout", "packed", "--csv", str(out))
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows = list(csv.DictReader(out.open()))
+    assert [int(x["message_count"]) for x in rows] == [100, 1 << 20]
+    assert all(x["backend"] == "cuda-packed" and int(x["repeats"]) >= 3 for x in rows)
+    # 2^20 x 64 B over PCIe and back: comfortably above 1 GB/s of hashed input
+    assert float(rows[1]["throughput_bps"]) > 1e9
+
+
+@pytest.mark.gpu
+def test_elapsed_is_the_wall_time_of_the_call(cli):
+    """BatchResult::elapsed (the bench's time_s) covers pack + copies + kernels + unpack; the
+    kernel-only time is a separate, much smaller column."""
+    r = run(cli, "bench", "--message-size", "64", "--sizes", "67108864")
+    assert r.returncode == 0, r.stdout + r.stderr
+    cols = r.stdout.strip().splitlines()[-1].split()
+    time_s, kernels_s = float(cols[4]), float(cols[7])
+    assert 0 < kernels_s < time_s
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo,bits,size", [("sha3-256", 0, 0), ("sha3-512", 0, 5_000_001), ("shake128", 2048, 777),
+                                            ("SHA3_224", 0, 4 << 20), ("shake-256", 0, 136)])
+def test_hash_subcommand(cli, tmp_path, algo, bits, size):
+    """`hash FILE` streams the file through the device-resident incremental hasher."""
+    import hashlib
+    import numpy as np
+    data = np.random.default_rng(size).integers(0, 256, size, dtype=np.uint8).tobytes()
+    f = tmp_path / "blob.bin"
+    f.write_bytes(data)
+    args = ["hash", "--algo", algo] + (["--bits", str(bits)] if bits else []) + [str(f)]
+    r = run(cli, *args)
+    assert r.returncode == 0, r.stdout + r.stderr
+    name = algo.lower().replace("-", "_").replace("shake_", "shake")
+    name = {"shake128": "shake_128", "shake256": "shake_256"}.get(name, name)
+    h = hashlib.new(name, data)
+    if name.startswith("shake"):
+        want = h.hexdigest((bits or (256 if name == "shake_128" else 512)) // 8)
+    else:
+        want = h.hexdigest()
+    assert r.stdout.strip() == want
+    assert run(cli, "hash", "--algo", "sha3-256", "--bits", "256", str(f)).returncode == 2
+    assert run(cli, "hash", str(tmp_path / "missing")).returncode == 3
+
+
+@pytest.mark.gpu
+def test_reference_parser_on_our_backend(tmp_path):
+    """The reference's unmodified vectors.cpp (parser) + the drop-in hash_batch: every response
+    file verifies through the GPU (oracle/_ref/ref_runner_on_b200 vectors ...)."""
+    tool = ROOT / "oracle" / "_ref" / "ref_runner_on_b200"
+    if not tool.exists():
+        pytest.skip("oracle/_ref/ref_runner_on_b200 not built (needs /root/reference at build time)")
+    files = []
+    total = 0
+    for kat in sorted(GOLDEN.glob("*.kat")):
+        dst = tmp_path / (kat.stem + ".rsp")
+        total += write_rsp(kat, dst)
+        files.append(str(dst))
+    r = subprocess.run([str(tool), "vectors", *files], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    seen = sum(int(row.rsplit(" ", 1)[1].split("/")[0]) for row in r.stdout.strip().splitlines())
+    assert seen == total == 892
