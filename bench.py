@@ -49,6 +49,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
     ap.add_argument("--no-dropin", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the cfg1..cfg4 device-time points")
+    ap.add_argument("--quick-configs", action="store_true", help=argparse.SUPPRESS)
     # validation only (one-GPU box): run N ranks on the SAME device with a gloo process group
     # to exercise the multi-rank code path; numbers from such a run are not benchmark values
     ap.add_argument("--share-gpu", action="store_true", help=argparse.SUPPRESS)
@@ -148,16 +150,119 @@ def measured_peaks():
 
 
 def ncu_traffic_per_launch(count_per_launch: int):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture, scaled
-    to this launch's message count (traffic is linear in messages); None if not captured."""
+    """(dram bytes per launch of the dominant kernel, where the figure comes from): the committed
+    `ncu --set full` capture of this command (profiles/roofline_traffic.json, made by
+    tools/ncu_traffic.py).  Used as captured when the capture's launch size equals this run's,
+    scaled per message otherwise; (None, reason) if there is no capture."""
     path = ROOT / "profiles" / "roofline_traffic.json"
     if not path.exists():
-        return None
+        return None, "no ncu capture committed"
     try:
         d = json.loads(path.read_text())
-        return d["dram_bytes_per_message"] * count_per_launch
+        if d["messages_per_launch"] == count_per_launch:
+            return d["dram_bytes_read_per_launch"] + d["dram_bytes_write_per_launch"], d["source"]
+        return (d["dram_bytes_per_message"] * count_per_launch,
+                d["source"] + f" scaled from {d['messages_per_launch']} messages per launch")
     except (ValueError, KeyError):
+        return None, "profiles/roofline_traffic.json unreadable"
+
+
+def executed_instr_per_hash(kernel: str):
+    """LOP3+SHF instructions one thread EXECUTES per hash in the built kernel, from the SASS
+    census (tools/sass_census.py -> profiles/sass_census.json); None if not generated."""
+    path = ROOT / "profiles" / "sass_census.json"
+    try:
+        return json.loads(path.read_text())[kernel]["executed_per_thread"]["LOP3+SHF"]
+    except (OSError, ValueError, KeyError):
         return None
+
+
+# --------------------------------------------------------------------------
+def config_points(engine, peak_instr_per_s: float, hbm_peak_gbs: float, quick: bool = False):
+    """Device-time points for BASELINE.json configs[0..3] (the headline line is configs[4]):
+    median of 5 launches after 2 warm-ups, CUDA events around the kernels on the launching
+    stream (cfg.device_ms), inputs resident in HBM and (except cfg1, see its note) larger than
+    L2.  `quick` shrinks every batch 64x (the CPU-side contract test of the record shape)."""
+    import torch
+
+    from paper_1902_05320_b200 import digest_bytes, permutations, selected_kernel
+
+    shrink = 6 if quick else 0
+    points = []
+
+    def record(name, alg, count, msg_bytes, perms, ms, kernel, **extra):
+        out_bytes = count * extra["digest_bytes"]
+        rate = perms / ms * 1e3
+        points.append({"config": name, "algorithm": alg, "messages": count, **extra, "ms": ms,
+                       "hashes_per_s": count / ms * 1e3, "gb_per_s_hashed": msg_bytes / ms / 1e6,
+                       "perms_per_s": rate, "int_roofline_frac": rate * INSTR_PER_PERMUTATION / peak_instr_per_s,
+                       "hbm_gb_per_s": (msg_bytes + out_bytes) / ms / 1e6,
+                       "hbm_frac": (msg_bytes + out_bytes) / ms / 1e6 / hbm_peak_gbs, "kernel": kernel})
+
+    def median_ms(run, reps=5, warm=2):
+        for _ in range(warm):
+            run()
+        return statistics.median(run() for _ in range(reps))
+
+    def fixed(name, alg, log2_count, msg_len, bits, back_to_back=0):
+        count = 1 << (log2_count - shrink)
+        data = engine.generate_workload(count * msg_len, msg_len, seed=1)
+        nbytes = digest_bytes(alg, bits)
+        out = torch.empty((count, nbytes), dtype=torch.uint8, device="cuda")
+        extra = {}
+        if back_to_back:
+            # sub-millisecond launch (SURVEY.md 8(d)): a train of launches between two events
+            # on the launching stream, per-launch steady state
+            for _ in range(8):
+                engine.hash_fixed(alg, data, msg_len, count, bits, out=out)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            trains = []
+            for _ in range(3):
+                e0.record()
+                for _ in range(back_to_back):
+                    engine.hash_fixed(alg, data, msg_len, count, bits, out=out)
+                e1.record()
+                e1.synchronize()
+                trains.append(e0.elapsed_time(e1) / back_to_back)
+            ms = statistics.median(trains)
+            extra = {"launches_per_train": back_to_back,
+                     "l2": "working set (%.0f MiB) fits the 126 MB L2: steady-state launches re-read an "
+                           "L2-resident input; the kernel is ALU-bound either way" % (count * (msg_len + nbytes) / 2**20)}
+        else:
+            def run():
+                engine.hash_fixed(alg, data, msg_len, count, bits, out=out, timed=True)
+                return engine.last_device_ms
+            ms = median_ms(run)
+        record(name, alg, count, count * msg_len, count * permutations(alg, msg_len, bits), ms,
+               selected_kernel(alg, msg_len, bits), msg_len=msg_len, xof_bits=bits, digest_bytes=nbytes, **extra)
+
+    fixed("cfg1: 2^20 x 64 B", "sha3_256", 20, 64, 0, back_to_back=200 if not quick else 20)
+    for alg, msg_len in (("sha3_224", 128), ("sha3_384", 256), ("sha3_512", 1024)):
+        fixed("cfg2: 2^24 fixed-length", alg, 24, msg_len, 0)
+    for alg, bits in (("shake128", 1024), ("shake256", 4096)):
+        fixed("cfg3: 2^24 x 64 B XOF", alg, 24, 64, bits)
+
+    # cfg4: 2^22 messages, lengths uniform 1..16384 (SURVEY.md 8(d): seed_len 2), 8-byte aligned
+    # starts, bucketed by block count on the device
+    count = 1 << (22 - shrink)
+    lengths = engine.generate_lengths(count, 1, 16384, seed_len=2)
+    padded = (lengths + 7) // 8 * 8
+    offsets = torch.cumsum(padded, 0) - padded
+    data = torch.empty(int(padded.sum().item()) + 16, dtype=torch.uint8, device="cuda")
+    engine.fill_messages(data, offsets, lengths, seed=1)
+    out = torch.empty((count, 32), dtype=torch.uint8, device="cuda")
+    msg_bytes = int(lengths.sum().item())
+    perms = int((lengths // 136 + 1).sum().item())
+
+    def run():
+        engine.hash_batch("sha3_256", data, offsets, lengths, out=out, timed=True)
+        return engine.last_device_ms
+    ms = median_ms(run, reps=3, warm=1)
+    record("cfg4: 2^22 x 1 B..16 KiB", "sha3_256", count, msg_bytes, perms, ms, selected_kernel("sha3_256", None, 0),
+           digest_bytes=32, mean_len=msg_bytes / count, metadata_bytes_per_message=16,
+           launches_per_call=engine.last_kernel_launches,
+           note="device time of the whole call: bucketing passes (histogram, scan, scatter) + hash kernel")
+    return points
 
 
 # --------------------------------------------------------------------------
@@ -173,19 +278,33 @@ def cpu_baseline(log2_messages: int, steps: int, warmup: int):
     from paper_1902_05320_b200.sharding import workload_slice
     data = workload_slice(total_bytes, MSG_LEN, 0, count, seed=1)
     cores = os.cpu_count() or 1
+    variants = {}
     if Reference.available():
-        ref = Reference()
-        cores = ref.hardware_workers()
-        batch = Reference.Batch(ref, 1, data, MSG_LEN, count)
-        times = [batch.run(parallel=True, workers=0) for _ in range(warmup + steps)][warmup:]
-        seq_count = min(count, 1 << 20)
-        seq_batch = Reference.Batch(ref, 1, data[:seq_count * MSG_LEN], MSG_LEN, seq_count)
-        seq = [seq_batch.run(parallel=False) for _ in range(3)]
-        batch.close()
-        seq_batch.close()
+        # Both builds of the reference (oracle/Makefile): "as_shipped" = batch.cpp:108 calling
+        # hash_one (one allocated digest vector per message, what the source asks for);
+        # "hash_into" = the same line hashing into the pre-sized slot (BASELINE.md section 3's
+        # one-line change, made by oracle/ref_prelude.hpp).  The FASTER one is the baseline.
+        seq_rate = None
+        for name, hash_into in (("as_shipped", False), ("hash_into", True)):
+            if not Reference.available(hash_into):
+                continue
+            ref = Reference(hash_into)
+            cores = ref.hardware_workers()
+            batch = Reference.Batch(ref, 1, data, MSG_LEN, count)
+            runs = [batch.run(parallel=True, workers=0) for _ in range(warmup + steps)][warmup:]
+            batch.close()
+            variants[name] = runs
+            if seq_rate is None:
+                seq_count = min(count, 1 << 20)
+                seq_batch = Reference.Batch(ref, 1, data[:seq_count * MSG_LEN], MSG_LEN, seq_count)
+                seq = [seq_batch.run(parallel=False) for _ in range(3)]
+                seq_batch.close()
+                seq_rate = seq_count / statistics.median(seq)
+        best = min(variants, key=lambda k: statistics.median(variants[k]))
+        times = variants[best]
         kind = "reference"
-        seq_rate = seq_count / statistics.median(seq)
     else:
+        best = "oracle port"
         t = []
         for _ in range(warmup + steps):
             t0 = time.perf_counter()
@@ -200,6 +319,8 @@ def cpu_baseline(log2_messages: int, steps: int, warmup: int):
     return {"value": count / med, "unit": "hashes/s", "cores": cores, "kind": kind,
             "sample": f"first 2^{log2_messages} messages of the same stream, hash_batch "
                       f"Backend::parallel workers={cores}, median of {steps} runs after {warmup} warm-up",
+            "build": best,
+            "builds_hashes_per_s": {k: count / statistics.median(v) for k, v in variants.items()},
             "ms_per_run": med * 1e3, "sequential_1core_hashes_per_s": seq_rate}, med
 
 
@@ -388,6 +509,9 @@ def main():
             probe = {"instr_per_s": rate, "sm_hz": hz}
         peak = probe["instr_per_s"] / 1e12 if probe else nominal_peak
         per_launch = count
+        kernel_name = "hash_oneblock_kernel<17, 8, 8, 23, 0u>"
+        executed = executed_instr_per_hash(kernel_name)
+        traffic, traffic_source = ncu_traffic_per_launch(per_launch)
         line = {
             "metric": METRIC, "value": value, "unit": "hashes/s", "n_gpus": world,
             "steps": args.steps, "warmup": warmup, "ms_per_step": seconds / args.steps * 1e3,
@@ -398,7 +522,7 @@ def main():
                                    f"over {world} GPU(s) by contiguous ranges (BASELINE.json configs[4])",
                        "messages_total": total, "messages_per_gpu": count, "message_bytes": MSG_LEN,
                        "l2_policy": "inputs larger than L2 (%.1f GiB per GPU per step)" % (count * MSG_LEN / 2**30),
-                       "kernel": "hash_oneblock_kernel<17,8,8,UNROLL=23 (peeled 1+7x3+2),ALU-only>"},
+                       "kernel": kernel_name + " (UNROLL 23 = peeled 1 + 7x3 + 2 rounds, ALU only)"},
             "gb_per_s_hashed": value * MSG_LEN / 1e9,
             "gpu_launches": launches,
             "digest_checksum": f"{checksum:016x}",
@@ -406,10 +530,18 @@ def main():
             "roofline": {
                 "bound": "int_alu",
                 "achieved": achieved, "peak": peak, "unit": "Tinstr/s", "frac": achieved / peak,
-                "traffic": ncu_traffic_per_launch(per_launch),
+                "traffic": traffic, "traffic_source": traffic_source,
+                "algorithmic_bytes_per_launch": per_launch * (MSG_LEN + DIGEST_BYTES),
+                "instr_per_hash_contract": INSTR_PER_PERMUTATION,
+                "instr_executed_per_hash": executed,
+                "frac_executed": (achieved * executed / INSTR_PER_PERMUTATION / peak) if executed else None,
                 "note": "per GPU; achieved = permutations/s x 4320 LOP3+SHF thread-instructions "
-                        "(SURVEY.md 8(d)); peak = LOP3+SHF issue rate measured in this run by "
-                        "b200sha3_probe_pipe" + ("" if probe else " [probe skipped: nominal]"),
+                        "(SURVEY.md 8(d)'s contract figure); peak = LOP3+SHF issue rate measured in this "
+                        "run by b200sha3_probe_pipe" + ("" if probe else " [probe skipped: nominal]") +
+                        ".  frac can read above 1 because the built kernel executes fewer than 4320 "
+                        "(instr_executed_per_hash, from the SASS census: ptxas removes dead work in "
+                        "rounds 0 and 23); frac_executed is the share of the pipe's issue slots the "
+                        "kernel actually fills",
                 "peak_nominal": nominal_peak,
                 "probe_sm_mhz": probe["sm_hz"] / 1e6 if probe else None,
             },
@@ -427,8 +559,12 @@ def main():
             dropin = dropin_cpp_wall()
             if dropin:
                 line["dropin_cpp"] = dropin
+        if world == 1 and not args.no_configs:
+            del data, digests
+            torch.cuda.empty_cache()
+            line["configs"] = config_points(engine, peak * 1e12, hbm_peak, quick=args.quick_configs)
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"], _ = cpu_baseline(args.cpu_log2_messages, 5, 1)
+            line["cpu_baseline"], _ = cpu_baseline(args.cpu_log2_messages, 5, 2)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -100,7 +100,8 @@ enum {
  * the reference's EngineConfig (batch.hpp:15-19): `workers`/`chunk_size` have
  * no meaning on a GPU and are replaced by device / stream / kernel knobs. */
 typedef struct b200sha3_config {
-  uint32_t struct_size;    /* sizeof(b200sha3_config), for ABI growth; 0 = this version */
+  uint32_t struct_size;    /* sizeof(b200sha3_config) the caller was built with; 0 = this
+                              version.  Fields beyond it are not read (ABI growth).      */
   int32_t device;          /* CUDA device ordinal; -1 = current device              */
   void* stream;            /* cudaStream_t to enqueue on; NULL = the default stream */
   uint32_t flags;          /* B200SHA3_FLAG_*                                        */
@@ -109,9 +110,8 @@ typedef struct b200sha3_config {
   int32_t fma_preset;      /* -1 = default; 0..8 = FMA-pipe rotation offload preset  */
   int32_t block_threads;   /* 0 = default                                            */
   /* If non-NULL receives the device time of the hashing phase in milliseconds
-   * (CUDA events around the kernels; copies excluded) -- what the adapter
-   * reports as BatchResult::elapsed (batch.cpp:84, :133).  Forces the call to
-   * wait for completion. */
+   * (CUDA events around the kernels; copies excluded) -- the adapter's
+   * StageTimes::kernels.  Forces the call to wait for completion. */
   double* device_ms;
   /* If non-NULL receives how many kernels this call launched. */
   uint32_t* kernel_launches;
@@ -130,6 +130,13 @@ B200SHA3_API uint32_t b200sha3_rate_bytes(int algorithm);
  * permutations plus max(0, ceil(digest_bytes/rate) - 1) squeeze permutations. */
 B200SHA3_API uint64_t b200sha3_permutations(int algorithm, uint64_t msg_len,
                                             uint64_t xof_output_bits);
+
+/* Which kernel B200SHA3_KERNEL_AUTO runs for a batch of this shape on 16-byte aligned
+ * buffers: equal-length messages of `msg_len` bytes, or a variable-length batch when
+ * msg_len == UINT64_MAX.  A static string such as "hash_oneblock_kernel<17,8,8>"; ""
+ * for a bad id.  Introspection for reports (bench.py); never needed to hash. */
+B200SHA3_API const char* b200sha3_selected_kernel(int algorithm, uint64_t msg_len,
+                                                  uint64_t xof_output_bits);
 
 B200SHA3_API const char* b200sha3_strerror(int status);
 

@@ -22,6 +22,7 @@ import numpy as np
 HERE = pathlib.Path(__file__).resolve().parent
 ORACLE_SO = HERE / "liboracle.so"
 REF_SO = HERE / "_ref" / "libsha3kit_ref.so"
+REF_HASHINTO_SO = HERE / "_ref" / "libsha3kit_ref_hashinto.so"
 
 ALGORITHMS = ("sha3_224", "sha3_256", "sha3_384", "sha3_512", "shake128", "shake256")
 u8p = C.POINTER(C.c_uint8)
@@ -150,13 +151,16 @@ class Reference:
     """The compiled reference (kind = "reference" CPU baseline)."""
 
     @staticmethod
-    def available() -> bool:
-        return REF_SO.exists()
+    def available(hash_into: bool = False) -> bool:
+        return (REF_HASHINTO_SO if hash_into else REF_SO).exists()
 
-    def __init__(self):
-        if not REF_SO.exists():
-            raise FileNotFoundError(f"{REF_SO} not built (needs /root/reference; see oracle/Makefile)")
-        self.lib = lib = C.CDLL(str(REF_SO))
+    def __init__(self, hash_into: bool = False):
+        """hash_into=True loads the build whose parallel branch hashes into the pre-sized
+        slots (oracle/ref_prelude.hpp): the reference's best case as a CPU baseline."""
+        so = REF_HASHINTO_SO if hash_into else REF_SO
+        if not so.exists():
+            raise FileNotFoundError(f"{so} not built (needs /root/reference; see oracle/Makefile)")
+        self.lib = lib = C.CDLL(str(so))
         lib.ref_batch_create.argtypes = [C.c_int, u8p, u64p, u64p, C.c_uint64, C.c_uint64, C.c_uint64]
         lib.ref_batch_create.restype = C.c_void_p
         lib.ref_batch_run.argtypes = [C.c_void_p, C.c_int, C.c_uint, C.c_uint64, u8p,

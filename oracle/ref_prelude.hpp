@@ -8,12 +8,27 @@
 // as shipped.  Declaring it here (and defining it in ref_shim.cpp on top of the
 // reference's own one-shot functions) lets the UNMODIFIED source compile; no
 // reference file is copied or patched.
+//
+// Second build (-DREF_HASH_INTO, oracle/_ref/libsha3kit_ref_hashinto.so): the reference's
+// best case for the CPU baseline.  batch.cpp's sequential branch hashes straight into the
+// pre-sized slot (hash_into, batch.cpp:15-25, :88) while its parallel branch goes through
+// hash_one, i.e. one allocated vector per message.  BASELINE.md section 3 plans the one-line
+// change `hash_into(v, batch.xof_output_bits, batch.messages[i], result.digests[i]);` for
+// line 108; here the preprocessor makes it while the source stays untouched: the statement
+//     result.digests[i] = hash_one(batch, batch.messages[i]);
+// becomes a self-assignment (a no-op) followed by that hash_into call.
 #pragma once
 #include <cstdint>
 #include <vector>
 
+#ifdef REF_HASH_INTO
+#define hash_one(b, m) result.digests[i]; hash_into(v, (b).xof_output_bits, (m), result.digests[i])
+#endif
+
+#ifndef REF_HASH_INTO
 namespace sha3 {
 struct HashBatch;
 std::vector<std::uint8_t> hash_one(const HashBatch& batch,
                                    const std::vector<std::uint8_t>& message);
 }  // namespace sha3
+#endif

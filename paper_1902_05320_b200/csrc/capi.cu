@@ -245,6 +245,29 @@ uint64_t b200sha3_permutations(int algorithm, uint64_t msg_len, uint64_t xof_out
   return msg_len / rate + 1 + (out > rate ? (out - 1) / rate : 0);
 }
 
+const char* b200sha3_selected_kernel(int algorithm, uint64_t msg_len, uint64_t xof_output_bits) {
+  if (algorithm < 0 || algorithm > 5) return "";
+  const Variant& v = kVariants[algorithm];
+  const uint64_t digest_bytes = b200sha3_digest_bytes(algorithm, xof_output_bits);
+  const bool whole_bytes = last_byte_mask(algorithm, xof_output_bits) == 0xffu;
+  thread_local char name[96];
+  if (msg_len == UINT64_MAX) {  // run_batch_device: classification on the device
+    std::snprintf(name, sizeof name, "bucket_order + %shash_generic_kernel<%d>",
+                  whole_bytes && short_supported(v.rate_lanes, digest_bytes) ? "hash_short_kernel | " : "",
+                  v.rate_lanes);
+  } else if (whole_bytes && oneblock_supported(v.rate_lanes, msg_len, digest_bytes)) {  // run_fixed_slice
+    std::snprintf(name, sizeof name, "hash_oneblock_kernel<%d,%d,%d>", v.rate_lanes,
+                  static_cast<int>(msg_len / 8), static_cast<int>(digest_bytes / 4));
+  } else if (whole_bytes && msg_len < 8u * static_cast<uint64_t>(v.rate_lanes) &&
+             short_supported(v.rate_lanes, digest_bytes)) {
+    std::snprintf(name, sizeof name, "hash_short_fixed_kernel<%d,%d>", v.rate_lanes,
+                  static_cast<int>(digest_bytes / 4));
+  } else {
+    std::snprintf(name, sizeof name, "hash_generic_kernel<%d>", v.rate_lanes);
+  }
+  return name;
+}
+
 const char* b200sha3_strerror(int status) {
   switch (status) {
     case B200SHA3_OK: return "ok";

@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 #include <cstdio>
 
@@ -56,18 +57,24 @@ struct Config {
   uint32_t* kernel_launches = nullptr;
 };
 
+// Reads only the fields the caller's struct has: struct_size is the sizeof the caller was
+// built with (0 = this version), so an older, shorter struct leaves the later knobs at
+// their defaults instead of having bytes past its end interpreted.
 inline Config resolve(const b200sha3_config* cfg) {
   Config c;
   if (!cfg) return c;
-  c.device = cfg->device;
-  c.stream = static_cast<cudaStream_t>(cfg->stream);
-  c.flags = cfg->flags;
-  c.kernel = cfg->kernel;
-  c.unroll = cfg->unroll;
-  c.fma_preset = cfg->fma_preset;
-  c.block_threads = cfg->block_threads;
-  c.device_ms = cfg->device_ms;
-  c.kernel_launches = cfg->kernel_launches;
+  const size_t have = cfg->struct_size ? cfg->struct_size : sizeof(b200sha3_config);
+#define B200SHA3_FIELD(name) (offsetof(b200sha3_config, name) + sizeof(cfg->name) <= have)
+  if (B200SHA3_FIELD(device)) c.device = cfg->device;
+  if (B200SHA3_FIELD(stream)) c.stream = static_cast<cudaStream_t>(cfg->stream);
+  if (B200SHA3_FIELD(flags)) c.flags = cfg->flags;
+  if (B200SHA3_FIELD(kernel)) c.kernel = cfg->kernel;
+  if (B200SHA3_FIELD(unroll)) c.unroll = cfg->unroll;
+  if (B200SHA3_FIELD(fma_preset)) c.fma_preset = cfg->fma_preset;
+  if (B200SHA3_FIELD(block_threads)) c.block_threads = cfg->block_threads;
+  if (B200SHA3_FIELD(device_ms)) c.device_ms = cfg->device_ms;
+  if (B200SHA3_FIELD(kernel_launches)) c.kernel_launches = cfg->kernel_launches;
+#undef B200SHA3_FIELD
   return c;
 }
 
