@@ -81,7 +81,10 @@ enum {
    * (messages are then hashed in input order, one per thread). */
   B200SHA3_FLAG_NO_BUCKETING = 1u << 0,
   /* Host-buffer entries: do not chunk/overlap copies with compute. */
-  B200SHA3_FLAG_NO_PIPELINE = 1u << 1
+  B200SHA3_FLAG_NO_PIPELINE = 1u << 1,
+  /* KERNEL_AUTO: never pick the warp-per-state kernel, however few the messages
+   * (small batches then take the same kernels as large ones). */
+  B200SHA3_FLAG_NO_WARP_KERNEL = 1u << 2
 };
 
 /* Kernel selection for experiments; 0 picks the measured default. */
@@ -91,9 +94,12 @@ enum {
   B200SHA3_KERNEL_ONEBLOCK = 2,  /* specialised single-block kernel when it fits  */
   B200SHA3_KERNEL_LANESPLIT = 3, /* 5 threads per state + warp shuffles (kept for
                                     the measured comparison in DESIGN.md)         */
-  B200SHA3_KERNEL_STAGED = 4     /* generic kernel with rate blocks staged through
+  B200SHA3_KERNEL_STAGED = 4,    /* generic kernel with rate blocks staged through
                                     shared memory by bulk async copies (TMA); also
                                     kept for the measured comparison               */
+  B200SHA3_KERNEL_WARP = 5       /* one message per warp (25 lanes over 25 threads,
+                                    shuffles): AUTO picks it for batches of few
+                                    multi-block messages                           */
 };
 
 /* Optional per-call configuration; NULL means all defaults.  The analogue of

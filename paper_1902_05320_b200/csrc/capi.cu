@@ -6,6 +6,7 @@
 // variable-length batches.  No CPU hashing code exists in this library: if CUDA is
 // unusable every compute entry returns B200SHA3_ERR_CUDA.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "capi_common.cuh"
@@ -19,6 +20,19 @@ thread_local char g_last_error[kLastErrorSize] = "";
 constexpr int kDefaultUnrollOneblock = 23;  // peeled 1 + 7x3 + 2 (17 KB): 4.43 vs 4.37 G hash/s for 24
 constexpr int kDefaultFmaOneblock = 0;
 constexpr int kDefaultFmaGeneric = 0;
+
+// Batches of at most this many messages go to the warp-per-state kernel (kernel_warp.cu) when
+// they are multi-block: one warp per message then finishes a permutation in a quarter of the
+// time one thread needs, and the machine has warps to spare (592 SMSPs).  Above it the
+// shuffle unit saturates and one message per thread is faster again (DESIGN.md section 4,
+// tools/long_message_latency.py).  B200SHA3_WARP_KERNEL_MAX overrides it for experiments.
+uint64_t warp_kernel_max_count() {
+  static const uint64_t value = [] {
+    const char* env = std::getenv("B200SHA3_WARP_KERNEL_MAX");
+    return env ? std::strtoull(env, nullptr, 10) : 2816ull;
+  }();
+  return value;
+}
 }  // namespace
 
 char* last_error_buffer() { return g_last_error; }
@@ -85,9 +99,16 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
   int kernel = c.kernel;
   if (kernel == B200SHA3_KERNEL_AUTO) {
     kernel = fits_oneblock ? B200SHA3_KERNEL_ONEBLOCK : B200SHA3_KERNEL_GENERIC;
+    // few multi-block messages: latency of the sponge chain is all there is
+    if (count <= warp_kernel_max_count() && (c.flags & B200SHA3_FLAG_NO_WARP_KERNEL) == 0 &&
+        b200sha3_permutations(algorithm, msg_len, xof_bits) >= 2) {
+      kernel = B200SHA3_KERNEL_WARP;
+    }
   }
   cudaError_t err;
-  if (fits_short) {
+  if (kernel == B200SHA3_KERNEL_WARP) {
+    err = launch_hash_warp(args, plan, stream);
+  } else if (fits_short) {
     err = launch_hash_short_fixed(args, plan, stream);
   } else if (kernel == B200SHA3_KERNEL_ONEBLOCK) {
     if (!fits_oneblock) {
@@ -146,6 +167,30 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
                      uint64_t digest_bytes, uint8_t* d_digests, const Config& c,
                      cudaStream_t stream, uint32_t* launches, const BatchHints* hints) {
   const Variant& v = kVariants[algorithm];
+  // Few messages: one warp each, every warp resident at once -- no classification, no order.
+  if (c.kernel == B200SHA3_KERNEL_WARP ||
+      (c.kernel == B200SHA3_KERNEL_AUTO && count <= warp_kernel_max_count() &&
+       (c.flags & B200SHA3_FLAG_NO_WARP_KERNEL) == 0 && !(hints && hints->all_short))) {
+    if (count > 0x7fffffffull) {
+      set_error_text("warp-per-state kernel: too many messages for one launch");
+      return B200SHA3_ERR_UNSUPPORTED;
+    }
+    HashArgs args{};
+    args.data = d_data;
+    args.offsets = d_offsets;
+    args.lengths = d_lengths;
+    args.count = count;
+    args.digests = d_digests;
+    args.digest_bytes = digest_bytes;
+    args.head = v.head;
+    args.last_mask = last_byte_mask(algorithm, xof_bits);
+    LaunchPlan plan{};
+    plan.rate_lanes = v.rate_lanes;
+    const cudaError_t err = launch_hash_warp(args, plan, stream);
+    if (err != cudaSuccess) return cuda_fail(err, "hash kernel launch");
+    if (launches) *launches += 1;
+    return B200SHA3_OK;
+  }
   tune_mempool_once();
   const uint64_t kSlice = 1ull << 30;
   const bool short_shape = c.kernel == B200SHA3_KERNEL_AUTO && is_aligned(d_data, 8) &&
@@ -251,6 +296,8 @@ const char* b200sha3_selected_kernel(int algorithm, uint64_t msg_len, uint64_t x
   const uint64_t digest_bytes = b200sha3_digest_bytes(algorithm, xof_output_bits);
   const bool whole_bytes = last_byte_mask(algorithm, xof_output_bits) == 0xffu;
   thread_local char name[96];
+  // (the count is not part of the query: below warp_kernel_max_count() multi-block batches run
+  // hash_warp_kernel instead)
   if (msg_len == UINT64_MAX) {  // run_batch_device: classification on the device
     std::snprintf(name, sizeof name, "bucket_order + %shash_generic_kernel<%d>",
                   whole_bytes && short_supported(v.rate_lanes, digest_bytes) ? "hash_short_kernel | " : "",

@@ -82,6 +82,12 @@ cudaError_t launch_hash_lanesplit(const HashArgs& args, const LaunchPlan& plan,
                                   cudaStream_t stream);
 bool lanesplit_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
 
+// Warp-per-state kernel (kernel_warp.cu): one message per WARP, the 25 lanes spread over 25
+// threads and exchanged with shuffles -- ~4x lower latency per permutation, for batches too
+// small to fill the machine with one message per thread.  Any length / alignment / digest
+// size; args.order may be nullptr.
+cudaError_t launch_hash_warp(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
+
 // TMA-staged variant of the generic kernel (kernel_staged.cu); blocks are staged when the
 // data base is 16-byte aligned and message starts are 8-byte aligned (else direct loads).
 cudaError_t launch_hash_staged(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);

@@ -12,6 +12,20 @@ from conftest import all_kat_files, load_kat_file, xof_bits_for
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(scope="module", params=["auto", "no_warp_kernel"])
+def engine(request):
+    """Small-batch tests run twice: under the product default (batches of at most 3072
+    multi-block messages take the warp-per-state kernel) and with that kernel switched off,
+    so that the one-message-per-thread kernels see the same vectors.  Full-size tests use
+    `big_engine` (the default) once."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test selected but no CUDA device is visible")
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_WARP_KERNEL
+    return Engine(flags=FLAG_NO_WARP_KERNEL if request.param == "no_warp_kernel" else 0)
+
+
 def pack(messages, align=1, lead=0):
     """Packs messages into one buffer with every start at `lead` mod `align`."""
     lengths = np.array([len(m) for m in messages], dtype=np.uint64)
@@ -47,14 +61,16 @@ def device_digests(engine, algorithm, messages, bits=0, align=1, lead=0, **kw):
     return out.cpu().numpy()
 
 
-def test_native_library_is_loaded(engine):
+def test_native_library_is_loaded(big_engine):
+    engine = big_engine
     from paper_1902_05320_b200 import library_path
     maps = open("/proc/self/maps").read()
     assert str(library_path()) in maps
 
 
-def test_permutation_kat(engine, inline_kats, oracle):
+def test_permutation_kat(big_engine, inline_kats, oracle):
     """Keccak-f[1600](0) (test_keccak.cpp:456-466) and random states vs the oracle."""
+    engine = big_engine
     import torch
     rng = np.random.default_rng(11)
     states = rng.integers(0, 2**63, (1000, 25), dtype=np.uint64)
@@ -176,9 +192,10 @@ def test_fixed_length_batches(engine, oracle, algorithm, msg_len):
     assert (engine.hash_fixed(algorithm, host, msg_len, count, bits) == expect).all()
 
 
-def test_every_kernel_variant_agrees(engine, oracle):
+def test_every_kernel_variant_agrees(big_engine, oracle):
     """The tuning matrix (unroll x FMA-offload presets, one-block and generic)
     must be invisible in the digests."""
+    engine = big_engine
     import torch
     from paper_1902_05320_b200 import Engine
     from paper_1902_05320_b200.engine import KERNEL_GENERIC, KERNEL_ONEBLOCK
@@ -290,9 +307,10 @@ def test_staged_kernel(oracle, algorithm):
     assert (eng.hash_fixed(algorithm, dev, msg_len, count, bits).cpu().numpy() == want).all()
 
 
-def test_bucket_order_is_a_sorted_permutation(engine):
+def test_bucket_order_is_a_sorted_permutation(big_engine):
     """Device bucketing: every index exactly once, block counts non-increasing
     up to the bin width."""
+    engine = big_engine
     import torch
     lengths = engine.generate_lengths(200_000, 1, 16384, seed_len=2)
     order = engine.bucket_order("sha3_256", lengths).cpu().numpy().astype(np.int64)
@@ -334,9 +352,10 @@ def test_variable_length_workload_vs_oracle(engine, oracle):
     assert (data[off:off + n].cpu().numpy() == words).all()
 
 
-def test_full_size_properties_cfg1(engine, oracle):
+def test_full_size_properties_cfg1(big_engine, oracle):
     """cfg1 at full size (2^20 x 64 B): sampled digests vs the oracle, a checksum
     of all digests vs the oracle's, sharding invariance, and determinism."""
+    engine = big_engine
     import torch
     count, total = 1 << 20, 1 << 26
     dev = engine.generate_workload(total, 64, seed=1)
@@ -354,10 +373,11 @@ def test_full_size_properties_cfg1(engine, oracle):
         assert torch.equal(part, got[first:first + n])
 
 
-def test_large_batch_roundtrip_properties(engine, oracle):
+def test_large_batch_roundtrip_properties(big_engine, oracle):
     """2^24 x 64 B (1 GiB): no oracle pass over everything -- sample 4096
     messages against the oracle and check the one-block and generic kernels agree
     on all 2^24 digests."""
+    engine = big_engine
     import torch
     from paper_1902_05320_b200 import Engine
     from paper_1902_05320_b200.engine import KERNEL_GENERIC
@@ -372,9 +392,10 @@ def test_large_batch_roundtrip_properties(engine, oracle):
     assert (fast[idx.cuda()].cpu().numpy() == expect).all()
 
 
-def test_host_entry_pipelined_equals_single_shot(engine, oracle):
+def test_host_entry_pipelined_equals_single_shot(big_engine, oracle):
     """Host-buffer entry with and without the chunked copy/compute pipeline
     (3 x 64 MiB slots), pageable and pinned memory."""
+    engine = big_engine
     import torch
     from paper_1902_05320_b200 import Engine
     from paper_1902_05320_b200.engine import FLAG_NO_PIPELINE
@@ -392,8 +413,9 @@ def test_host_entry_pipelined_equals_single_shot(engine, oracle):
     assert (a[sample] == expect).all()
 
 
-def test_reentrant_from_multiple_callers(engine, oracle):
+def test_reentrant_from_multiple_callers(big_engine, oracle):
     """test_batch.cpp:178-196: three threads, each with its own batch call."""
+    engine = big_engine
     import threading
     rng = oracle.test_rng(54)
     msgs = [rng.random_bytes(rng.below(31)) for _ in range(200)]
@@ -410,7 +432,8 @@ def test_reentrant_from_multiple_callers(engine, oracle):
     assert all(ok)
 
 
-def test_xof_without_length_rejected_on_gpu_box_too(engine):
+def test_xof_without_length_rejected_on_gpu_box_too(big_engine):
+    engine = big_engine
     with pytest.raises(ValueError):
         engine.hash_messages("shake256", [b"\x01"], 0)
 
@@ -425,11 +448,12 @@ def _sample_check(oracle, algorithm, dev, msg_len, count, digests, bits=0, n=204
     assert (digests[idx].cpu().numpy() == expect).all()
 
 
-def test_cfg5_full_size_2pow28(engine, oracle):
+def test_cfg5_full_size_2pow28(big_engine, oracle):
     """configs[4]: SHA3-256 over 2^28 x 64 B (16 GiB in, 8 GiB out).  Two independent kernels
     (single-block, fully unrolled vs generic, rolled) agree on every digest; 2048 sampled
     messages match the oracle; eight independently generated shards reproduce the digests
     (the N-GPU invariance); the first message is the cfg1/cfg5 stream KAT."""
+    engine = big_engine
     import torch
     from paper_1902_05320_b200 import Engine
     from paper_1902_05320_b200.engine import KERNEL_GENERIC
@@ -455,9 +479,10 @@ def test_cfg5_full_size_2pow28(engine, oracle):
 
 @pytest.mark.parametrize("algorithm,msg_len,bits", [(0, 32, 0), (0, 1024, 0), (2, 256, 0), (3, 1024, 0),
                                                     (4, 64, 4096), (5, 64, 256), (5, 64, 2048)])
-def test_cfg2_cfg3_full_size_2pow24(engine, oracle, algorithm, msg_len, bits):
+def test_cfg2_cfg3_full_size_2pow24(big_engine, oracle, algorithm, msg_len, bits):
     """configs[1] / configs[2] at 2^24 messages: auto-selected kernel == generic kernel on all
     digests, sampled oracle check, XOF prefix property (shorter output is a prefix)."""
+    engine = big_engine
     import torch
     from paper_1902_05320_b200 import Engine
     from paper_1902_05320_b200.engine import KERNEL_GENERIC
@@ -473,10 +498,11 @@ def test_cfg2_cfg3_full_size_2pow24(engine, oracle, algorithm, msg_len, bits):
         assert torch.equal(short, got[:, :32])          # test_sha3.cpp:150-158 at scale
 
 
-def test_cfg4_full_size_2pow22(engine, oracle):
+def test_cfg4_full_size_2pow22(big_engine, oracle):
     """configs[3]: 2^22 messages, lengths 1..16 KiB (~34 GB): bucketed and unbucketed runs
     agree on every digest; 256 sampled messages match the oracle; digest slots follow input
     order although processing order is by block count."""
+    engine = big_engine
     import torch
     from paper_1902_05320_b200 import Engine
     from paper_1902_05320_b200.engine import FLAG_NO_BUCKETING
@@ -508,10 +534,11 @@ def test_one_huge_message_among_small_ones(engine):
     assert got == [hashlib.shake_128(m).digest(337) for m in msgs[1:3]]
 
 
-def test_variable_length_host_entry_pipelined(engine, oracle):
+def test_variable_length_host_entry_pipelined(big_engine, oracle):
     """Host entry, packed ragged batch of ~200 MB: chunked 3-slot pipeline == single shot ==
     oracle (sampled); a batch whose offsets are NOT in order falls back to the single-shot
     path and is still right; permuting the messages permutes the digests."""
+    engine = big_engine
     from paper_1902_05320_b200 import Engine
     from paper_1902_05320_b200.engine import FLAG_NO_PIPELINE
     rng = np.random.default_rng(12)
@@ -532,7 +559,8 @@ def test_variable_length_host_entry_pipelined(engine, oracle):
     assert (shuffled == piped[perm]).all()
 
 
-def test_pinned_alloc_api(engine):
+def test_pinned_alloc_api(big_engine):
+    engine = big_engine
     import ctypes as C
     lib = engine.lib
     lib.b200sha3_pinned_alloc.argtypes = [C.c_uint64, C.POINTER(C.c_void_p)]
@@ -550,11 +578,12 @@ def test_pinned_alloc_api(engine):
     assert lib.b200sha3_pinned_alloc(0, C.byref(p)) == 0 and not p.value
 
 
-def test_pageable_host_buffers_are_staged_through_the_bounce_ring(engine, oracle):
+def test_pageable_host_buffers_are_staged_through_the_bounce_ring(big_engine, oracle):
     """Host entries on ordinary (pageable) memory >= 4 MiB stage blocks through pinned bounce
     buffers with helper threads (csrc/capi_host.cu, BounceRing): every mix of pageable / pinned
     input and output, and a ragged batch whose offset / length tables are large enough to be
     staged too, must give the digests of the device-buffer entry."""
+    engine = big_engine
     import torch
     count = 700_001                     # 42.7 MiB in, 21.4 MiB out: several 8 MiB blocks, ragged tail
     dev = engine.generate_workload(count * 64, 64, seed=9, count=count)
@@ -614,12 +643,13 @@ def test_all_short_ragged_batches(engine, oracle, algorithm, bits):
 
 
 @pytest.mark.parametrize("algorithm,bits", [(0, 0), (1, 0), (2, 0), (3, 0), (4, 256), (5, 512), (5, 128), (4, 1000)])
-def test_equal_length_single_block_batches_of_every_length(engine, oracle, algorithm, bits):
+def test_equal_length_single_block_batches_of_every_length(big_engine, oracle, algorithm, bits):
     """Equal-length batches of every length 0 .. rate-1 (the paper's 10-byte messages among them,
     PAPER.md:307): lengths that are not 32 / 64 / 128 bytes go to hash_short_fixed_kernel
     (csrc/kernel_short.cu) with its uniform jump-table tails -- whole-lane loads when every
     start is 8-byte aligned, 4-byte loads + PRMT otherwise.  Device entry at three base
     alignments and the host entry, against the oracle."""
+    engine = big_engine
     import torch
     rate = oracle.rate_bytes(algorithm)
     rng = np.random.default_rng(200 + algorithm)
