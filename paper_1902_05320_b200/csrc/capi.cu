@@ -203,9 +203,11 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
   const bool bucketing = (c.flags & B200SHA3_FLAG_NO_BUCKETING) == 0 && !host_short && !host_plain;
   for (uint64_t first = 0; first < count; first += kSlice) {
     const uint32_t n = static_cast<uint32_t>(std::min<uint64_t>(kSlice, count - first));
-    uint32_t* scratch = nullptr;  // [0] unaligned flag, [1] ragged flag, then bucket scratch, then order
+    // [0] unaligned flag, [1] ragged flag, [2] long flag, then bucket scratch, then order
     const size_t words = 8 + kBucketScratchWords + (bucketing ? static_cast<size_t>(n) : 0);
-    CU(cudaMallocAsync(&scratch, words * sizeof(uint32_t), stream));
+    AsyncScratch scratch_memory;
+    CU(scratch_memory.alloc(words * sizeof(uint32_t), stream));
+    uint32_t* scratch = scratch_memory.as<uint32_t>();
     uint32_t* flag = scratch;
     uint32_t* bucket_scratch = scratch + 8;
     uint32_t* order = bucketing ? scratch + 8 + kBucketScratchWords : nullptr;
@@ -256,11 +258,7 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
                                                : launch_hash_generic(args, plan, stream);
       if (err == cudaSuccess && launches) *launches += 1;
     }
-    if (err != cudaSuccess) {
-      cudaFreeAsync(scratch, stream);
-      return cuda_fail(err, "hash kernel launch");
-    }
-    CU(cudaFreeAsync(scratch, stream));
+    if (err != cudaSuccess) return cuda_fail(err, "hash kernel launch");
   }
   return B200SHA3_OK;
 }
@@ -454,14 +452,14 @@ int b200sha3_bucket_order_device(int algorithm, const uint64_t* d_lengths, uint6
   DeviceGuard guard;
   CU(guard.enter(c.device));
   tune_mempool_once();
-  uint32_t* scratch = nullptr;
-  CU(cudaMallocAsync(&scratch, (8 + kBucketScratchWords) * sizeof(uint32_t), c.stream));
+  AsyncScratch scratch_memory;
+  CU(scratch_memory.alloc((8 + kBucketScratchWords) * sizeof(uint32_t), c.stream));
+  uint32_t* scratch = scratch_memory.as<uint32_t>();
   CU(cudaMemsetAsync(scratch, 0, 8 * sizeof(uint32_t), c.stream));
   // lengths double as "offsets" here: only their low bits feed the alignment flag
   CU(launch_bucket_order(d_lengths, d_lengths, static_cast<uint32_t>(count),
                          8u * kVariants[algorithm].rate_lanes, d_order, scratch + 8, scratch,
                          c.stream));
-  CU(cudaFreeAsync(scratch, c.stream));
   return B200SHA3_OK;
 }
 

@@ -130,6 +130,30 @@ class Timer {
   cudaEvent_t e0_ = nullptr, e1_ = nullptr;
 };
 
+// Stream-ordered scratch memory, returned to the pool when the scope ends -- on the error
+// paths too.
+class AsyncScratch {
+ public:
+  cudaError_t alloc(size_t bytes, cudaStream_t stream) {
+    stream_ = stream;
+    return cudaMallocAsync(&ptr_, bytes, stream);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(ptr_);
+  }
+  ~AsyncScratch() {
+    if (ptr_) cudaFreeAsync(ptr_, stream_);
+  }
+  AsyncScratch() = default;
+  AsyncScratch(const AsyncScratch&) = delete;
+  AsyncScratch& operator=(const AsyncScratch&) = delete;
+
+ private:
+  void* ptr_ = nullptr;
+  cudaStream_t stream_ = nullptr;
+};
+
 // Keeps stream-ordered allocations cached between calls (once per process).
 void tune_mempool_once();
 

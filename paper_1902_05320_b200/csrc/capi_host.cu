@@ -226,46 +226,61 @@ class ChunkPlanner {
     };
     // Strips of kStrip messages: the in-order test and the statistics of a strip are plain
     // reductions without early exits (this loop reads 16 bytes per message and, for 2^24 short
-    // messages, is what the copy engines wait for); a strip that is not in order is walked
-    // message by message to find where the order breaks.
+    // messages, is what the copy engines wait for).  A strip that is not in order, holds an
+    // empty message (whose offset means nothing and must not widen the byte range) or would
+    // overshoot the byte target (long messages) is walked message by message instead.
+    bool have_bytes = false;
     uint64_t i = next_;
     while (i < count_) {
       const uint64_t n = std::min<uint64_t>(kStrip, count_ - i);
       const uint64_t* off = offsets_ + i;
       const uint64_t* len = lengths_ + i;
-      uint64_t bad = (off[0] < prev_end_) | (off[0] + len[0] < off[0]);
+      uint64_t bad = (off[0] < prev_end_) | (off[0] + len[0] < off[0]) | (len[0] == 0);
       uint64_t strip_or = off[0], strip_max = len[0], strip_ne = len[0] ^ first_len;
       for (uint64_t k = 1; k < n; ++k) {
         const uint64_t end_before = off[k - 1] + len[k - 1];
-        bad |= (off[k] < end_before) | (off[k] + len[k] < off[k]);
+        bad |= (off[k] < end_before) | (off[k] + len[k] < off[k]) | (len[k] == 0);
         strip_or |= off[k];
         strip_max = std::max(strip_max, len[k]);
         strip_ne |= len[k] ^ first_len;
       }
-      if (bad) break;  // handled below, message by message
-      if (cur.count == 0) cur.lo = off[0] & ~15ull;
-      cur.count += n;
-      cur.hi = off[n - 1] + len[n - 1];
-      prev_end_ = cur.hi;
-      misaligned |= strip_or;
-      max_len = std::max(max_len, strip_max);
-      equal = equal && strip_ne == 0;
-      i += n;
-      if (cur.hi - cur.lo >= target_ || cur.count >= (1ull << 22)) return close(i);
-    }
-    for (; i < count_; ++i) {  // only reached inside a strip that breaks the order
-      const uint64_t len = lengths_[i], end = offsets_[i] + len;
-      if (offsets_[i] < prev_end_ || end < offsets_[i]) {  // out of order (or wrapping)
-        if (cur.count == 0) return rest(out);
-        return close(i);  // close the chunk in progress; the next call takes the rest
+      if (!bad) {
+        const uint64_t lo = have_bytes ? cur.lo : off[0] & ~15ull;
+        bad = off[n - 1] + len[n - 1] - lo > target_ + target_ / 4;  // close inside the strip
       }
-      if (cur.count == 0) cur.lo = offsets_[i] & ~15ull;
-      cur.count += 1;
-      cur.hi = end;
-      prev_end_ = end;
-      misaligned |= offsets_[i];
-      max_len = std::max(max_len, len);
-      equal = equal && len == first_len;
+      if (!bad) {
+        if (!have_bytes) cur.lo = off[0] & ~15ull;
+        have_bytes = true;
+        cur.count += n;
+        cur.hi = off[n - 1] + len[n - 1];
+        prev_end_ = cur.hi;
+        misaligned |= strip_or;
+        max_len = std::max(max_len, strip_max);
+        equal = equal && strip_ne == 0;
+        i += n;
+      } else {
+        for (const uint64_t strip_end = i + n; i < strip_end; ++i) {
+          const uint64_t length = lengths_[i], end = offsets_[i] + length;
+          equal = equal && length == first_len;
+          if (length == 0) {  // belongs to the chunk, touches no byte of `data`
+            cur.count += 1;
+            continue;
+          }
+          if (offsets_[i] < prev_end_ || end < offsets_[i]) {  // out of order (or wrapping)
+            if (cur.count == 0) return rest(out);
+            return close(i);  // close the chunk in progress; the next call takes the rest
+          }
+          if (!have_bytes) cur.lo = offsets_[i] & ~15ull;
+          have_bytes = true;
+          cur.count += 1;
+          cur.hi = end;
+          prev_end_ = end;
+          misaligned |= offsets_[i];
+          max_len = std::max(max_len, length);
+          if (cur.hi - cur.lo >= target_) return close(i + 1);
+        }
+      }
+      if ((have_bytes && cur.hi - cur.lo >= target_) || cur.count >= (1ull << 22)) return close(i);
     }
     return close(count_);
   }

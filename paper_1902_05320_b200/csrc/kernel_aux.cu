@@ -36,18 +36,27 @@ __global__ void __launch_bounds__(128) permute_kernel(uint64_t* states, uint64_t
 // of their absorb-block count, heaviest first, so that the threads of a warp
 // run (nearly) the same number of permutations.
 //
-// Key: the block count itself below 128, then 16 sub-bins per power of two
-// (<= 6.25 % spread inside a bin), clamped to 255 keys; stored inverted so
-// that key 0 is the heaviest bin.
+// Single-block messages (len < rate) are ordered too -- by their number of whole 32-bit
+// words: their cost does not differ, but a warp whose threads hold the SAME number of words
+// absorbs the final block through a jump table of statically indexed loads instead of
+// 2 x RL predicated ones (sponge.cuh: absorb_tail / absorb_tail_uniform_unaligned), which is
+// the difference between 0.90 and ~0.97 of the ALU roofline on short ragged batches.
+//
+// Key, 256 values, stored inverted so that key 0 is the heaviest bin:
+//   one block    its word count len >> 2                      (0 .. 41)
+//   2 .. 63      42 + block count                              (44 .. 105)
+//   >= 64        16 sub-bins per power of two (<= 6.25 % spread inside a bin), clamped
 __device__ __forceinline__ uint32_t bucket_key(uint64_t len, uint32_t rate_bytes) {
   const uint64_t blocks = len / rate_bytes + 1u;
   uint32_t key;
-  if (blocks < 128u) {
-    key = static_cast<uint32_t>(blocks);
+  if (blocks == 1u) {
+    key = static_cast<uint32_t>(len) >> 2;  // < 42: the largest rate is 168 bytes
+  } else if (blocks < 64u) {
+    key = 42u + static_cast<uint32_t>(blocks);
   } else {
-    const int e = 63 - __clzll(static_cast<long long>(blocks));  // >= 7
+    const int e = 63 - __clzll(static_cast<long long>(blocks));  // >= 6
     const uint32_t frac = static_cast<uint32_t>(blocks >> (e - 4)) & 15u;
-    key = 128u + static_cast<uint32_t>(e - 7) * 16u + frac;
+    key = 106u + static_cast<uint32_t>(e - 6) * 16u + frac;
     if (key > 255u) key = 255u;
   }
   return 255u - key;
@@ -117,9 +126,12 @@ __global__ void __launch_bounds__(kBucketThreads)
 bucket_scatter_kernel(const uint64_t* __restrict__ lengths, uint32_t count,
                       uint32_t rate_bytes, const uint32_t* __restrict__ bin_base,
                       uint32_t* __restrict__ cursor, uint32_t* __restrict__ order,
-                      const uint32_t* __restrict__ skip_flags) {
-  // an all-short batch goes to hash_short_kernel, which needs no order
-  if (skip_flags != nullptr && skip_flags[2] == 0u) return;
+                      const uint32_t* __restrict__ flags) {
+  // `flags` is given when hash_short_kernel is launched next: an all-short batch whose
+  // messages start on 8-byte boundaries is hashed there in input order (predicated 8-byte lane
+  // loads: 0.97 of the roofline; ordering it costs more in gathered loads than the uniform
+  // absorb saves), so no order is needed.
+  if (flags != nullptr && flags[2] == 0u && flags[0] == 0u) return;
   __shared__ uint32_t local[kBucketBins];   // per-block count, then block base
   for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) local[i] = 0u;
   __syncthreads();
@@ -253,7 +265,7 @@ cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream
 cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,
                                 uint32_t count, uint32_t rate_bytes, uint32_t* order,
                                 uint32_t* scratch, uint32_t* unaligned_flag,
-                                cudaStream_t stream, bool skip_order_if_short) {
+                                cudaStream_t stream, bool short_kernel_next) {
   if (count == 0) return cudaSuccess;
   uint32_t* hist = scratch;
   uint32_t* cursor = scratch + kBucketBins;
@@ -266,7 +278,7 @@ cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths
                                                                 unaligned_flag);
   bucket_scan_kernel<<<1, kBucketBins, 0, stream>>>(hist, cursor);
   bucket_scatter_kernel<<<blocks, kBucketThreads, 0, stream>>>(
-      lengths, count, rate_bytes, hist, cursor, order, skip_order_if_short ? unaligned_flag : nullptr);
+      lengths, count, rate_bytes, hist, cursor, order, short_kernel_next ? unaligned_flag : nullptr);
   return cudaGetLastError();
 }
 

@@ -6,9 +6,10 @@
 // lanes (zero before the first permutation) or on the lanes nobody reads after the last one,
 // the block-count loop, the processing order.  When the classification pass
 // (kernel_aux.cu) finds no message of a whole block, this kernel does the batch instead
-// (8-byte aligned starts: 8-byte loads; any other layout: aligned 4-byte loads + PRMT): predicated lane loads straight into a zero state
-// (absorb_tail, ragged form), the peeled permutation of the one-block kernel
-// (1 + 7x3 + 2 rounds), OW digest words out, input order.  It is launched next to the
+// (8-byte aligned starts: 8-byte loads; any other layout: aligned 4-byte loads + PRMT): lane
+// loads straight into a zero state, the peeled permutation of the one-block kernel
+// (1 + 7x3 + 2 rounds), OW digest words out; messages taken in the order of the bucketing pass
+// (by word count) when there is one, else in input order.  It is launched next to the
 // generic kernel; each of the two returns at once when the flags give the batch to the other.
 #include "kernels.cuh"
 #include "sponge.cuh"
@@ -17,7 +18,13 @@ namespace b200sha3 {
 
 namespace {
 
-template <int RL, int OW>
+// The final block is absorbed by the predicated "ragged" form (~6 ALU instructions per lane on
+// 8-byte aligned starts: 0.97 of the roofline in input order).  Starts at odd addresses cost
+// ~10 per lane that way (0.90), so for those -- SORTED -- args.order lists the messages by
+// their number of whole 32-bit words (the bucketing pass, kernel_aux.cu): the threads of a
+// warp then hold final blocks of the same shape (all but the warps that straddle two bins) and
+// the jump table of statically indexed 4-byte loads + PRMT applies (0.94 including the pass).
+template <int RL, int OW, bool SORTED>
 __global__ void __launch_bounds__(256)
 hash_short_kernel(const HashArgs args) {
   static_assert(OW <= 2 * RL, "digest must fit one block");
@@ -27,13 +34,19 @@ hash_short_kernel(const HashArgs args) {
   // 0.921 vs 0.957 of the roofline on 2^24 x 0..135 B.)
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (tid >= args.count) return;
-  const uint8_t* p = args.data + args.offsets[tid];
-  const uint32_t len = static_cast<uint32_t>(args.lengths[tid]);  // < 8 * RL
+  const bool sorted = SORTED && !aligned8;  // (the bucketing pass writes no order for aligned batches)
+  const uint64_t m = sorted ? static_cast<uint64_t>(args.order[tid]) : tid;
+  const uint8_t* p = args.data + args.offsets[m];
+  const uint32_t len = static_cast<uint32_t>(args.lengths[m]);  // < 8 * RL
   State a;
   state_zero(a);
-  absorb_tail<RL>(a, p, len, args.head, aligned8, /*ragged=*/true);
+  if (sorted) {
+    absorb_tail_uniform_unaligned<RL>(a, p, len, args.head);
+  } else {
+    absorb_tail<RL>(a, p, len, args.head, aligned8, /*ragged=*/true);
+  }
   keccak_f1600<23, 0u>(a);  // peeled 1 + 7x3 + 2
-  emit_block<RL>(a, args.digests + tid * (4u * OW), 4u * OW);
+  emit_block<RL>(a, args.digests + m * (4u * OW), 4u * OW);
 }
 
 // The same for EQUAL-LENGTH batches of any length below the rate -- what the one-block kernel
@@ -77,7 +90,11 @@ cudaError_t launch_instance(const HashArgs& args, const LaunchPlan& plan, cudaSt
   const uint64_t blocks = (args.count + threads - 1) / threads;
   if (blocks == 0) return cudaSuccess;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
-  hash_short_kernel<RL, OW><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(args);
+  if (args.order) {
+    hash_short_kernel<RL, OW, true><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(args);
+  } else {
+    hash_short_kernel<RL, OW, false><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(args);
+  }
   return cudaGetLastError();
 }
 

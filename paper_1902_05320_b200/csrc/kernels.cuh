@@ -95,18 +95,20 @@ cudaError_t launch_hash_staged(const HashArgs& args, const LaunchPlan& plan, cud
 // Keccak-f[1600] on raw 200-byte states (test hook).
 cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream);
 
-// Bucketing by block count: writes a processing order (heaviest first), sets
-// *unaligned_flag if any offset is not a multiple of 8, unaligned_flag[1] (the "ragged"
-// word) if the messages do not all leave the same number of bytes for the final block and
-// unaligned_flag[2] (the "long" word) if some message is at least one rate block long -- in
-// which case only the ordering is computed at all.
+// Bucketing: writes a processing order -- by block count, heaviest first, single-block
+// messages by their number of whole 32-bit words -- sets *unaligned_flag if any offset is not
+// a multiple of 8, unaligned_flag[1] (the "ragged" word) if the messages do not all leave the
+// same number of bytes for the final block and unaligned_flag[2] (the "long" word) if some
+// message is at least one rate block long.  With `short_kernel_next` (hash_short_kernel is
+// launched after this pass) the order is left unwritten for a batch of single-block messages
+// with 8-byte aligned starts: that kernel takes those in input order.
 // `scratch` needs kBucketScratchWords 32-bit words.
 constexpr int kBucketBins = 256;
 constexpr int kBucketScratchWords = 2 * kBucketBins + 8;
 cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,
                                 uint32_t count, uint32_t rate_bytes, uint32_t* order,
                                 uint32_t* scratch, uint32_t* unaligned_flag,
-                                cudaStream_t stream, bool skip_order_if_short = false);
+                                cudaStream_t stream, bool short_kernel_next = false);
 // The two flag words only (no ordering).
 cudaError_t launch_alignment_check(const uint64_t* offsets, const uint64_t* lengths, uint64_t count,
                                    uint32_t rate_bytes, uint32_t* unaligned_flag, cudaStream_t stream);

@@ -127,3 +127,37 @@ def test_misc_queries_without_a_device():
     assert lib.b200sha3_states_create(7, 4, None, C.byref(handle)) == 1 and not handle.value
     lib.b200sha3_states_destroy.argtypes = [C.c_void_p]
     assert lib.b200sha3_states_destroy(None) == 0
+
+
+def test_short_config_struct_is_honoured():
+    """b200sha3_config::struct_size is the size the CALLER was built with: fields beyond it are
+    never read.  A caller with a struct that ends before the two result pointers leaves garbage
+    there; the library must not write through it (count == 0 returns before any CUDA call)."""
+    from paper_1902_05320_b200.engine import _Config, _library
+    lib = _library()
+    cfg = _Config()
+    ctypes.memset(ctypes.byref(cfg), 0xEE, ctypes.sizeof(cfg))   # every later field: garbage
+    cfg.struct_size = _Config.device_ms.offset                   # an older, shorter struct
+    cfg.device, cfg.stream, cfg.flags, cfg.kernel = -1, None, 0, 0
+    cfg.unroll, cfg.fma_preset, cfg.block_threads = 0, -1, 0
+    assert lib.b200sha3_hash_fixed_device(1, None, 64, 0, 0, None, ctypes.byref(cfg)) == 0
+    assert lib.b200sha3_hash_batch(1, None, None, None, 0, 0, None, ctypes.byref(cfg)) == 0
+    # struct_size 0 means "this version": the pointers are used
+    ms, launches = ctypes.c_double(7.0), ctypes.c_uint32(7)
+    cfg.struct_size = 0
+    cfg.device_ms, cfg.kernel_launches = ctypes.pointer(ms), ctypes.pointer(launches)
+    assert lib.b200sha3_hash_fixed_device(1, None, 64, 0, 0, None, ctypes.byref(cfg)) == 0
+    assert ms.value == 0.0 and launches.value == 0
+
+
+def test_selected_kernel_names():
+    """Which kernel KERNEL_AUTO runs per shape (reports only; no GPU needed to ask)."""
+    from paper_1902_05320_b200 import selected_kernel
+    assert selected_kernel("sha3_256", 64) == "hash_oneblock_kernel<17,8,8>"
+    assert selected_kernel("sha3_256", 10) == "hash_short_fixed_kernel<17,8>"
+    assert selected_kernel("sha3_512", 1024) == "hash_generic_kernel<9>"
+    assert selected_kernel("shake128", 64, 1023) == "hash_generic_kernel<21>"     # odd bits: masked tail
+    assert selected_kernel("shake128", 64, 1024) == "hash_oneblock_kernel<21,8,32>"
+    assert "hash_short_kernel" in selected_kernel("sha3_256", None)
+    assert "hash_short_kernel" not in selected_kernel("shake256", None, 4099)
+    assert selected_kernel(9, 64) == ""

@@ -308,16 +308,27 @@ def test_staged_kernel(oracle, algorithm):
 
 
 def test_bucket_order_is_a_sorted_permutation(big_engine):
-    """Device bucketing: every index exactly once, block counts non-increasing
-    up to the bin width."""
+    """Device bucketing: every index exactly once; keys non-increasing, the key being the block
+    count below 64 blocks, 16 sub-bins per power of two above, and -- among single-block
+    messages -- the number of whole 32-bit words (kernel_aux.cu: bucket_key)."""
     engine = big_engine
     import torch
-    lengths = engine.generate_lengths(200_000, 1, 16384, seed_len=2)
-    order = engine.bucket_order("sha3_256", lengths).cpu().numpy().astype(np.int64)
-    assert np.array_equal(np.sort(order), np.arange(200_000))
-    blocks = (lengths.cpu().numpy() // 136 + 1)[order]
-    assert blocks[0] == blocks.max() and blocks[-1] == blocks.min()
-    assert (np.diff(blocks) <= 0).all()      # below 128 blocks every bin is one block count
+
+    def key(lengths):
+        blocks = lengths // 136 + 1
+        e = np.floor(np.log2(np.maximum(blocks, 1))).astype(np.int64)
+        coarse = 106 + (e - 6) * 16 + ((blocks >> np.maximum(e - 4, 0)) & 15)
+        return np.where(blocks == 1, lengths >> 2, np.where(blocks < 64, 42 + blocks, np.minimum(coarse, 255)))
+
+    for lo, hi in ((1, 16384), (0, 135), (0, 400)):
+        lengths = engine.generate_lengths(200_000, lo, hi, seed_len=2)
+        order = engine.bucket_order("sha3_256", lengths).cpu().numpy().astype(np.int64)
+        assert np.array_equal(np.sort(order), np.arange(200_000))
+        host = lengths.cpu().numpy()
+        keys = key(host)[order]
+        assert (np.diff(keys) <= 0).all()
+        blocks = (host // 136 + 1)[order]
+        assert blocks[0] >= blocks.max() - 3 and blocks[-1] == blocks.min()   # 64..127 blocks: bins of 4
     torch.cuda.synchronize()
 
 
@@ -665,3 +676,55 @@ def test_equal_length_single_block_batches_of_every_length(big_engine, oracle, a
         host = engine.hash_fixed(algorithm, data[:max(count * msg_len, 1)], msg_len, count, bits)
         assert (host == oracle.hash_batch(algorithm, data[:count * msg_len], fixed_len=msg_len, count=count,
                                           xof_bits=bits, workers=4)).all(), (msg_len, "host")
+
+
+def test_empty_messages_do_not_widen_the_host_range(big_engine, oracle):
+    """An empty message's offset means nothing: it must not extend the byte range the host
+    entry copies (offsets far outside the buffer, NULL data with all-empty batches)."""
+    import ctypes as C
+    engine = big_engine
+    data = np.frombuffer(b"0123456789", dtype=np.uint8).copy()
+    offsets = np.array([0, 1 << 40, 3, (1 << 63) + 5], dtype=np.uint64)
+    lengths = np.array([10, 0, 4, 0], dtype=np.uint64)
+    got = engine.hash_batch("sha3_256", data, offsets, lengths)
+    expect = [oracle.hash_one(1, m) for m in (b"0123456789", b"", b"3456", b"")]
+    assert [g.tobytes() for g in got] == expect
+    # the same shape inside a long in-order batch (the strip fast path must notice the empty one)
+    n = 5000
+    lengths = np.full(n, 7, dtype=np.uint64)
+    offsets = np.arange(n, dtype=np.uint64) * np.uint64(7)
+    lengths[1234] = 0
+    offsets[1234] = np.uint64(1 << 50)
+    blob = np.random.default_rng(1).integers(0, 256, 7 * n, dtype=np.uint8)
+    got = engine.hash_batch("sha3_224", blob, offsets, lengths)
+    for i in (0, 1233, 1234, 1235, n - 1):
+        m = blob[int(offsets[i]):int(offsets[i]) + int(lengths[i])].tobytes() if lengths[i] else b""
+        assert got[i].tobytes() == oracle.hash_one(0, m)
+    # all-empty batch with NULL data and arbitrary offsets
+    out = np.zeros((3, 32), dtype=np.uint8)
+    offs = np.array([5, 1 << 44, 77], dtype=np.uint64)
+    lens = np.zeros(3, dtype=np.uint64)
+    rc = engine.lib.b200sha3_hash_batch(1, None, offs.ctypes.data, lens.ctypes.data, 3, 0, out.ctypes.data, None)
+    assert rc == 0 and all(out[i].tobytes() == oracle.hash_one(1, b"") for i in range(3))
+
+
+def test_long_messages_are_cut_into_chunks_by_bytes(big_engine):
+    """Fewer than 1024 messages but more than the 1 GiB chunk target: the host entry must
+    close chunks by BYTES (copy / compute overlap, bounded device staging), digests unchanged."""
+    import hashlib
+    engine = big_engine
+    rng = np.random.default_rng(12)
+    n = 700
+    lengths = rng.integers(2_000_000, 2_400_000, n).astype(np.uint64)          # ~1.5 GB in all
+    offsets = np.concatenate([[0], np.cumsum((lengths + 7) // 8 * 8)[:-1]]).astype(np.uint64)
+    total = int(offsets[-1] + lengths[-1])
+    blob = rng.integers(0, 2**63, total // 8 + 2, dtype=np.uint64).view(np.uint8)
+    got = engine.hash_batch("sha3_256", blob, offsets, lengths)
+    assert engine.last_kernel_launches >= 2                                    # more than one chunk
+    for i in (0, 1, 299, 480, 698, 699):
+        m = blob[int(offsets[i]):int(offsets[i] + lengths[i])].tobytes()
+        assert got[i].tobytes() == hashlib.sha3_256(m).digest()
+    import torch
+    dev = engine.hash_batch("sha3_256", torch.from_numpy(blob).cuda(), torch.from_numpy(offsets.view(np.int64)).cuda(),
+                            torch.from_numpy(lengths.view(np.int64)).cuda())
+    assert (dev.cpu().numpy() == got).all()

@@ -34,6 +34,8 @@ for log2_count, max_len in [(22, 300), (22, 1000), (20, 300), (24, 135), (22, 40
         rec[name] = {"device_ms": best, "gperm_per_s": perms / best / 1e6,
                      "int_roofline_frac": perms / (best * 1e-3) * 4320 / peak}
     out.append(rec)
-    print(json.dumps(rec), flush=True)
+    print(f"align {pack}: 2^{log2_count} x 0..{max_len} B  bucketed {rec['bucketed']['int_roofline_frac']:.3f} "
+          f"({rec['bucketed']['device_ms']:.3f} ms)  input order {rec['input_order']['int_roofline_frac']:.3f} "
+          f"({rec['input_order']['device_ms']:.3f} ms)", flush=True)
 (ROOT / "gpurun_out").mkdir(exist_ok=True)
 (ROOT / "gpurun_out" / f"short_ragged_align{pack}.json").write_text(json.dumps(out, indent=1))
