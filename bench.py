@@ -234,7 +234,8 @@ def config_points(engine, peak_instr_per_s: float, hbm_peak_gbs: float, quick: b
                 return engine.last_device_ms
             ms = median_ms(run)
         record(name, alg, count, count * msg_len, count * permutations(alg, msg_len, bits), ms,
-               selected_kernel(alg, msg_len, bits), msg_len=msg_len, xof_bits=bits, digest_bytes=nbytes, **extra)
+               selected_kernel(alg, msg_len, bits, count), msg_len=msg_len, xof_bits=bits, digest_bytes=nbytes,
+               **extra)
 
     fixed("cfg1: 2^20 x 64 B", "sha3_256", 20, 64, 0, back_to_back=200 if not quick else 20)
     for alg, msg_len in (("sha3_224", 128), ("sha3_384", 256), ("sha3_512", 1024)):
@@ -258,10 +259,34 @@ def config_points(engine, peak_instr_per_s: float, hbm_peak_gbs: float, quick: b
         engine.hash_batch("sha3_256", data, offsets, lengths, out=out, timed=True)
         return engine.last_device_ms
     ms = median_ms(run, reps=3, warm=1)
-    record("cfg4: 2^22 x 1 B..16 KiB", "sha3_256", count, msg_bytes, perms, ms, selected_kernel("sha3_256", None, 0),
+    record("cfg4: 2^22 x 1 B..16 KiB", "sha3_256", count, msg_bytes, perms, ms,
+           selected_kernel("sha3_256", None, 0, count),
            digest_bytes=32, mean_len=msg_bytes / count, metadata_bytes_per_message=16,
            launches_per_call=engine.last_kernel_launches,
            note="device time of the whole call: bucketing passes (histogram, scan, scatter) + hash kernel")
+    del data, out, offsets, lengths, padded
+    torch.cuda.empty_cache()
+
+    # Beyond BASELINE.json's configs: few long messages, where the sponge chain's latency is all
+    # there is (one warp per message, csrc/kernel_warp.cu) -- next to the same batch with one
+    # message per thread.
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_WARP_KERNEL
+    count, msg_len = (1024, 1 << 20) if not quick else (64, 1 << 16)
+    data = engine.generate_workload(count * msg_len, msg_len, seed=1)
+    out = torch.empty((count, 32), dtype=torch.uint8, device="cuda")
+    per_thread = Engine(device=engine.device, flags=FLAG_NO_WARP_KERNEL)
+    times = {}
+    for name, eng in (("warp", engine), ("thread", per_thread)):
+        def run():
+            eng.hash_fixed("sha3_256", data, msg_len, count, out=out, timed=True)
+            return eng.last_device_ms
+        times[name] = median_ms(run, reps=3, warm=1)
+    record("few long messages: 1024 x 1 MiB", "sha3_256", count, count * msg_len,
+           count * permutations("sha3_256", msg_len), times["warp"], selected_kernel("sha3_256", msg_len, 0, count),
+           msg_len=msg_len, xof_bits=0, digest_bytes=32, ms_one_message_per_thread=times["thread"],
+           note="latency-bound (a sponge is sequential per message): the roofline fraction says how much of the "
+                "machine 1024 messages can use, not how good the kernel is")
     return points
 
 

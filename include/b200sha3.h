@@ -138,10 +138,10 @@ B200SHA3_API uint64_t b200sha3_permutations(int algorithm, uint64_t msg_len,
                                             uint64_t xof_output_bits);
 
 /* Which kernel B200SHA3_KERNEL_AUTO runs for a batch of this shape on 16-byte aligned
- * buffers: equal-length messages of `msg_len` bytes, or a variable-length batch when
+ * buffers: `count` equal-length messages of `msg_len` bytes, or a variable-length batch when
  * msg_len == UINT64_MAX.  A static string such as "hash_oneblock_kernel<17,8,8>"; ""
  * for a bad id.  Introspection for reports (bench.py); never needed to hash. */
-B200SHA3_API const char* b200sha3_selected_kernel(int algorithm, uint64_t msg_len,
+B200SHA3_API const char* b200sha3_selected_kernel(int algorithm, uint64_t msg_len, uint64_t count,
                                                   uint64_t xof_output_bits);
 
 B200SHA3_API const char* b200sha3_strerror(int status);

@@ -288,15 +288,17 @@ uint64_t b200sha3_permutations(int algorithm, uint64_t msg_len, uint64_t xof_out
   return msg_len / rate + 1 + (out > rate ? (out - 1) / rate : 0);
 }
 
-const char* b200sha3_selected_kernel(int algorithm, uint64_t msg_len, uint64_t xof_output_bits) {
+const char* b200sha3_selected_kernel(int algorithm, uint64_t msg_len, uint64_t count,
+                                     uint64_t xof_output_bits) {
   if (algorithm < 0 || algorithm > 5) return "";
   const Variant& v = kVariants[algorithm];
   const uint64_t digest_bytes = b200sha3_digest_bytes(algorithm, xof_output_bits);
   const bool whole_bytes = last_byte_mask(algorithm, xof_output_bits) == 0xffu;
   thread_local char name[96];
-  // (the count is not part of the query: below warp_kernel_max_count() multi-block batches run
-  // hash_warp_kernel instead)
-  if (msg_len == UINT64_MAX) {  // run_batch_device: classification on the device
+  const bool few = count <= warp_kernel_max_count();
+  if (few && (msg_len == UINT64_MAX || b200sha3_permutations(algorithm, msg_len, xof_output_bits) >= 2)) {
+    std::snprintf(name, sizeof name, "hash_warp_kernel");  // run_fixed_slice / run_batch_device
+  } else if (msg_len == UINT64_MAX) {  // run_batch_device: classification on the device
     std::snprintf(name, sizeof name, "bucket_order + %shash_generic_kernel<%d>",
                   whole_bytes && short_supported(v.rate_lanes, digest_bytes) ? "hash_short_kernel | " : "",
                   v.rate_lanes);

@@ -75,7 +75,7 @@ def _load() -> C.CDLL:
     lib.b200sha3_rate_bytes.restype = C.c_uint32
     lib.b200sha3_permutations.argtypes = [C.c_int, C.c_uint64, C.c_uint64]
     lib.b200sha3_permutations.restype = C.c_uint64
-    lib.b200sha3_selected_kernel.argtypes = [C.c_int, C.c_uint64, C.c_uint64]
+    lib.b200sha3_selected_kernel.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64]
     lib.b200sha3_selected_kernel.restype = C.c_char_p
     lib.b200sha3_strerror.argtypes = [C.c_int]
     lib.b200sha3_strerror.restype = C.c_char_p
@@ -150,11 +150,11 @@ def permutations(algorithm, msg_len: int, xof_output_bits: int = 0) -> int:
     return int(_library().b200sha3_permutations(algorithm_id(algorithm), msg_len, xof_output_bits))
 
 
-def selected_kernel(algorithm, msg_len: int | None, xof_output_bits: int = 0) -> str:
-    """Name of the kernel KERNEL_AUTO picks for equal-length messages of msg_len bytes (None:
-    a variable-length batch) on aligned buffers."""
+def selected_kernel(algorithm, msg_len: int | None, xof_output_bits: int = 0, count: int = 1 << 24) -> str:
+    """Name of the kernel KERNEL_AUTO picks for `count` equal-length messages of msg_len bytes
+    (None: a variable-length batch) on aligned buffers."""
     n = (1 << 64) - 1 if msg_len is None else msg_len
-    return _library().b200sha3_selected_kernel(algorithm_id(algorithm), n, xof_output_bits).decode()
+    return _library().b200sha3_selected_kernel(algorithm_id(algorithm), n, count, xof_output_bits).decode()
 
 
 def _is_torch(x) -> bool:

@@ -161,3 +161,8 @@ def test_selected_kernel_names():
     assert "hash_short_kernel" in selected_kernel("sha3_256", None)
     assert "hash_short_kernel" not in selected_kernel("shake256", None, 4099)
     assert selected_kernel(9, 64) == ""
+    # few multi-block messages: one warp per message
+    assert selected_kernel("sha3_256", 1 << 20, count=1024) == "hash_warp_kernel"
+    assert selected_kernel("sha3_256", None, count=100) == "hash_warp_kernel"
+    assert selected_kernel("sha3_256", 64, count=100) == "hash_oneblock_kernel<17,8,8>"   # single block
+    assert selected_kernel("sha3_256", 1 << 20, count=1 << 14) == "hash_generic_kernel<17>"

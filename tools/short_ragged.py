@@ -16,7 +16,7 @@ probe = Engine(device=0)
 peak, _ = probe.probe_pipe(2)
 out = []
 pack = int(sys.argv[1]) if len(sys.argv) > 1 else 8      # message starts are multiples of this
-for log2_count, max_len in [(22, 300), (22, 1000), (20, 300), (24, 135), (22, 4096)]:
+for log2_count, max_len in [(22, 300), (22, 1000), (20, 300), (24, 135), (22, 135), (22, 4096)]:
     count = 1 << log2_count
     g = torch.Generator(device="cuda").manual_seed(3)
     lengths = torch.randint(0, max_len + 1, (count,), generator=g, device="cuda", dtype=torch.int64)
