@@ -154,6 +154,15 @@ class AsyncScratch {
   cudaStream_t stream_ = nullptr;
 };
 
+// A second stream (plus the two events of a fork / join) next to the caller's, cached per calling
+// thread and device: run_batch_device launches the two alternative hash kernels of a
+// variable-length batch side by side, so that the one that returns at once costs nothing.
+struct SideLane {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+cudaError_t side_lane(SideLane* out);
+
 // Keeps stream-ordered allocations cached between calls (once per process).
 void tune_mempool_once();
 

@@ -46,8 +46,17 @@ __global__ void __launch_bounds__(128) permute_kernel(uint64_t* states, uint64_t
 //   one block    its word count len >> 2                      (0 .. 41)
 //   2 .. 63      42 + block count                              (44 .. 105)
 //   >= 64        16 sub-bins per power of two (<= 6.25 % spread inside a bin), clamped
-__device__ __forceinline__ uint32_t bucket_key(uint64_t len, uint32_t rate_bytes) {
-  const uint64_t blocks = len / rate_bytes + 1u;
+// RATE is a template argument: the block count is a division by a compile-time constant
+// (multiply + shift) -- with a run-time divisor the two 64-bit divisions per message made
+// these passes compute bound (84 us for 2^24 messages against 45 us of memory traffic).
+template <uint32_t RATE>
+__device__ __forceinline__ uint64_t whole_blocks(uint64_t len) {
+  return (len >> 32) == 0 ? static_cast<uint64_t>(static_cast<uint32_t>(len) / RATE) : len / RATE;
+}
+
+template <uint32_t RATE>
+__device__ __forceinline__ uint32_t bucket_key(uint64_t len) {
+  const uint64_t blocks = whole_blocks<RATE>(len) + 1u;
   uint32_t key;
   if (blocks == 1u) {
     key = static_cast<uint32_t>(len) >> 2;  // < 42: the largest rate is 168 bytes
@@ -62,54 +71,58 @@ __device__ __forceinline__ uint32_t bucket_key(uint64_t len, uint32_t rate_bytes
   return 255u - key;
 }
 
+// Sets flags[0] / [1] / [2] if any thread of the warp saw a misaligned start / a different tail
+// length / a message of a whole block.  The words only ever go from 0 to 1, so a warp looks
+// before it writes: in a ragged batch EVERY warp has something to report, and 65536 atomics on
+// one address (2^24 messages) cost more than reading the batch (116 us against 45).
+__device__ __forceinline__ void raise_flags(uint32_t* flags, uint32_t misaligned, uint32_t ragged,
+                                            uint32_t has_long) {
+  const bool report[3] = {__any_sync(0xffffffffu, misaligned != 0u) != 0, __any_sync(0xffffffffu, ragged != 0u) != 0,
+                          __any_sync(0xffffffffu, has_long != 0u) != 0};
+  if ((threadIdx.x & 31) != 0) return;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (report[k] && *reinterpret_cast<volatile uint32_t*>(flags + k) == 0u) atomicOr(flags + k, 1u);
+  }
+}
+
 constexpr int kBucketThreads = 256;
 constexpr int kBucketItems = 8;  // messages per thread
+static_assert(kBucketThreads == kBucketBins, "one thread per bin in the block-level steps");
 
 // scratch layout: [0,256) histogram / bin base, [256,512) running cursor,
 // [512] unused.
+template <uint32_t RATE>
 __global__ void __launch_bounds__(kBucketThreads)
 bucket_histogram_kernel(const uint64_t* __restrict__ offsets,
                         const uint64_t* __restrict__ lengths, uint32_t count,
-                        uint32_t rate_bytes, uint32_t* __restrict__ hist,
-                        uint32_t* __restrict__ unaligned_flag) {
+                        uint32_t* __restrict__ hist, uint32_t* __restrict__ unaligned_flag) {
   __shared__ uint32_t local[kBucketBins];
-  for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) local[i] = 0u;
+  local[threadIdx.x] = 0u;
   __syncthreads();
   const uint32_t base = blockIdx.x * (kBucketThreads * kBucketItems);
-  const uint32_t first_tail = static_cast<uint32_t>(lengths[0] % rate_bytes);
+  const uint64_t len0 = lengths[0];
+  const uint32_t first_tail = static_cast<uint32_t>(len0 - whole_blocks<RATE>(len0) * RATE);
   uint32_t misaligned = 0u, ragged = 0u, has_long = 0u;
 #pragma unroll
   for (int k = 0; k < kBucketItems; ++k) {
     const uint32_t i = base + k * kBucketThreads + threadIdx.x;
     if (i < count) {
       const uint64_t len = lengths[i];
-      atomicAdd(&local[bucket_key(len, rate_bytes)], 1u);
+      atomicAdd(&local[bucket_key<RATE>(len)], 1u);
       misaligned |= static_cast<uint32_t>(offsets[i]) & 7u;
-      ragged |= static_cast<uint32_t>(len % rate_bytes) ^ first_tail;
-      has_long |= len >= rate_bytes ? 1u : 0u;
+      ragged |= static_cast<uint32_t>(len - whole_blocks<RATE>(len) * RATE) ^ first_tail;
+      has_long |= len >= RATE ? 1u : 0u;
     }
   }
-  if (__any_sync(0xffffffffu, misaligned != 0u) && (threadIdx.x & 31) == 0) {
-    atomicOr(unaligned_flag, 1u);
-  }
-  if (__any_sync(0xffffffffu, ragged != 0u) && (threadIdx.x & 31) == 0) {
-    atomicOr(unaligned_flag + 1, 1u);
-  }
-  if (__any_sync(0xffffffffu, has_long != 0u) && (threadIdx.x & 31) == 0) {
-    atomicOr(unaligned_flag + 2, 1u);
-  }
+  raise_flags(unaligned_flag, misaligned, ragged, has_long);
   __syncthreads();
-  for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) {
-    if (local[i]) atomicAdd(&hist[i], local[i]);
-  }
+  if (local[threadIdx.x]) atomicAdd(&hist[threadIdx.x], local[threadIdx.x]);
 }
 
-// Exclusive scan of the 256 bins (one block): hist -> bin base; cursor <- 0.
-__global__ void __launch_bounds__(kBucketBins)
-bucket_scan_kernel(uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor) {
-  __shared__ uint32_t tmp[kBucketBins];
+// Exclusive scan of kBucketBins values held one per thread (whole block, kBucketBins threads).
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t mine, uint32_t* tmp) {
   const int t = threadIdx.x;
-  const uint32_t mine = hist[t];
   tmp[t] = mine;
   __syncthreads();
   for (int d = 1; d < kBucketBins; d <<= 1) {
@@ -118,67 +131,86 @@ bucket_scan_kernel(uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor) {
     tmp[t] += add;
     __syncthreads();
   }
-  hist[t] = tmp[t] - mine;
-  cursor[t] = 0u;
+  return tmp[t] - mine;
 }
 
+// Exclusive scan of the 256 bins (one block): hist -> bin base; cursor <- 0.
+__global__ void __launch_bounds__(kBucketBins)
+bucket_scan_kernel(uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor) {
+  __shared__ uint32_t tmp[kBucketBins];
+  hist[threadIdx.x] = block_exclusive_scan(hist[threadIdx.x], tmp);
+  cursor[threadIdx.x] = 0u;
+}
+
+// A block ranks its 2048 messages inside their bins (shared-memory counters), reserves a run
+// of every bin it touches (one global atomic per bin), lays the message indices out bin by bin
+// in shared memory and writes them from there: consecutive threads then write consecutive
+// entries of `order`.  (Writing order[base + rank] straight from the ranking loop sent the 32
+// stores of a warp to up to 32 different bins: 105 us for 2^24 messages.)
+template <uint32_t RATE>
 __global__ void __launch_bounds__(kBucketThreads)
 bucket_scatter_kernel(const uint64_t* __restrict__ lengths, uint32_t count,
-                      uint32_t rate_bytes, const uint32_t* __restrict__ bin_base,
-                      uint32_t* __restrict__ cursor, uint32_t* __restrict__ order,
-                      const uint32_t* __restrict__ flags) {
+                      const uint32_t* __restrict__ bin_base, uint32_t* __restrict__ cursor,
+                      uint32_t* __restrict__ order, const uint32_t* __restrict__ flags) {
   // `flags` is given when hash_short_kernel is launched next: an all-short batch whose
   // messages start on 8-byte boundaries is hashed there in input order (predicated 8-byte lane
   // loads: 0.97 of the roofline; ordering it costs more in gathered loads than the uniform
   // absorb saves), so no order is needed.
   if (flags != nullptr && flags[2] == 0u && flags[0] == 0u) return;
-  __shared__ uint32_t local[kBucketBins];   // per-block count, then block base
-  for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) local[i] = 0u;
+  constexpr int kTile = kBucketThreads * kBucketItems;
+  __shared__ uint32_t local[kBucketBins];     // per-block count of the bin
+  __shared__ uint32_t tmp[kBucketBins];
+  __shared__ uint32_t tile_index[kTile];      // message index, bin by bin
+  __shared__ uint32_t tile_target[kTile];     // where it goes in `order`
+  local[threadIdx.x] = 0u;
   __syncthreads();
-  const uint32_t base = blockIdx.x * (kBucketThreads * kBucketItems);
+  const uint32_t base = blockIdx.x * kTile;
   uint32_t key[kBucketItems], rank[kBucketItems];
 #pragma unroll
   for (int k = 0; k < kBucketItems; ++k) {
     const uint32_t i = base + k * kBucketThreads + threadIdx.x;
     if (i < count) {
-      key[k] = bucket_key(lengths[i], rate_bytes);
+      key[k] = bucket_key<RATE>(lengths[i]);
       rank[k] = atomicAdd(&local[key[k]], 1u);
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kBucketBins; i += blockDim.x) {
-    const uint32_t n = local[i];
-    local[i] = n ? bin_base[i] + atomicAdd(&cursor[i], n) : 0u;
-  }
+  const uint32_t n = local[threadIdx.x];
+  const uint32_t in_tile = block_exclusive_scan(n, tmp);  // (ends with a barrier)
+  const uint32_t in_order = n ? bin_base[threadIdx.x] + atomicAdd(&cursor[threadIdx.x], n) : 0u;
+  __shared__ uint32_t tile_start[kBucketBins], order_start[kBucketBins];
+  tile_start[threadIdx.x] = in_tile;
+  order_start[threadIdx.x] = in_order;
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < kBucketItems; ++k) {
     const uint32_t i = base + k * kBucketThreads + threadIdx.x;
-    if (i < count) order[local[key[k]] + rank[k]] = i;
+    if (i < count) {
+      const uint32_t q = tile_start[key[k]] + rank[k];
+      tile_index[q] = i;
+      tile_target[q] = order_start[key[k]] + rank[k];
+    }
   }
+  __syncthreads();
+  const uint32_t tile_count = count - base < static_cast<uint32_t>(kTile) ? count - base : kTile;
+  for (uint32_t q = threadIdx.x; q < tile_count; q += kBucketThreads) order[tile_target[q]] = tile_index[q];
 }
 
+template <uint32_t RATE>
 __global__ void __launch_bounds__(256)
 alignment_check_kernel(const uint64_t* __restrict__ offsets, const uint64_t* __restrict__ lengths,
-                       uint64_t count, uint32_t rate_bytes, uint32_t* __restrict__ unaligned_flag) {
-  const uint32_t first_tail = static_cast<uint32_t>(lengths[0] % rate_bytes);
+                       uint64_t count, uint32_t* __restrict__ unaligned_flag) {
+  const uint64_t len0 = lengths[0];
+  const uint32_t first_tail = static_cast<uint32_t>(len0 - whole_blocks<RATE>(len0) * RATE);
   uint32_t misaligned = 0u, ragged = 0u, has_long = 0u;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t len = lengths[i];
     misaligned |= static_cast<uint32_t>(offsets[i]) & 7u;
-    ragged |= static_cast<uint32_t>(len % rate_bytes) ^ first_tail;
-    has_long |= len >= rate_bytes ? 1u : 0u;
+    ragged |= static_cast<uint32_t>(len - whole_blocks<RATE>(len) * RATE) ^ first_tail;
+    has_long |= len >= RATE ? 1u : 0u;
   }
-  if (__any_sync(0xffffffffu, has_long != 0u) && (threadIdx.x & 31) == 0) {
-    atomicOr(unaligned_flag + 2, 1u);
-  }
-  if (__any_sync(0xffffffffu, misaligned != 0u) && (threadIdx.x & 31) == 0) {
-    atomicOr(unaligned_flag, 1u);
-  }
-  if (__any_sync(0xffffffffu, ragged != 0u) && (threadIdx.x & 31) == 0) {
-    atomicOr(unaligned_flag + 1, 1u);
-  }
+  raise_flags(unaligned_flag, misaligned, ragged, has_long);
 }
 
 // ---------------------------------------------------------------------------
@@ -262,32 +294,65 @@ cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream
   return cudaGetLastError();
 }
 
-cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,
-                                uint32_t count, uint32_t rate_bytes, uint32_t* order,
-                                uint32_t* scratch, uint32_t* unaligned_flag,
-                                cudaStream_t stream, bool short_kernel_next) {
-  if (count == 0) return cudaSuccess;
+namespace {
+
+template <uint32_t RATE>
+cudaError_t bucket_order_for_rate(const uint64_t* offsets, const uint64_t* lengths, uint32_t count,
+                                  uint32_t* order, uint32_t* scratch, uint32_t* unaligned_flag,
+                                  cudaStream_t stream, bool short_kernel_next) {
   uint32_t* hist = scratch;
   uint32_t* cursor = scratch + kBucketBins;
   cudaError_t err = cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * kBucketScratchWords, stream);
   if (err != cudaSuccess) return err;
   const unsigned per_block = kBucketThreads * kBucketItems;
   const unsigned blocks = (count + per_block - 1) / per_block;
-  bucket_histogram_kernel<<<blocks, kBucketThreads, 0, stream>>>(offsets, lengths, count,
-                                                                rate_bytes, hist,
-                                                                unaligned_flag);
+  bucket_histogram_kernel<RATE><<<blocks, kBucketThreads, 0, stream>>>(offsets, lengths, count, hist,
+                                                                      unaligned_flag);
   bucket_scan_kernel<<<1, kBucketBins, 0, stream>>>(hist, cursor);
-  bucket_scatter_kernel<<<blocks, kBucketThreads, 0, stream>>>(
-      lengths, count, rate_bytes, hist, cursor, order, short_kernel_next ? unaligned_flag : nullptr);
+  bucket_scatter_kernel<RATE><<<blocks, kBucketThreads, 0, stream>>>(
+      lengths, count, hist, cursor, order, short_kernel_next ? unaligned_flag : nullptr);
   return cudaGetLastError();
 }
+
+}  // namespace
+
+// One instantiation per sponge rate (sha3.cpp:13-20).
+#define B200SHA3_FOR_RATE(RATE_BYTES, CALL)      \
+  switch (RATE_BYTES) {                          \
+    case 72u: return CALL(72u);                  \
+    case 104u: return CALL(104u);                \
+    case 136u: return CALL(136u);                \
+    case 144u: return CALL(144u);                \
+    case 168u: return CALL(168u);                \
+    default: return cudaErrorInvalidValue;       \
+  }
+
+cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,
+                                uint32_t count, uint32_t rate_bytes, uint32_t* order,
+                                uint32_t* scratch, uint32_t* unaligned_flag,
+                                cudaStream_t stream, bool short_kernel_next) {
+  if (count == 0) return cudaSuccess;
+#define B200SHA3_CALL(R) \
+  bucket_order_for_rate<R>(offsets, lengths, count, order, scratch, unaligned_flag, stream, short_kernel_next)
+  B200SHA3_FOR_RATE(rate_bytes, B200SHA3_CALL)
+#undef B200SHA3_CALL
+}
+
+namespace {
+template <uint32_t RATE>
+cudaError_t alignment_check_for_rate(const uint64_t* offsets, const uint64_t* lengths, uint64_t count,
+                                     uint32_t* unaligned_flag, cudaStream_t stream) {
+  alignment_check_kernel<RATE><<<grid_for(count, 256), 256, 0, stream>>>(offsets, lengths, count, unaligned_flag);
+  return cudaGetLastError();
+}
+}  // namespace
 
 cudaError_t launch_alignment_check(const uint64_t* offsets, const uint64_t* lengths, uint64_t count,
                                    uint32_t rate_bytes, uint32_t* unaligned_flag, cudaStream_t stream) {
   if (count == 0) return cudaSuccess;
-  alignment_check_kernel<<<grid_for(count, 256), 256, 0, stream>>>(offsets, lengths, count, rate_bytes,
-                                                                  unaligned_flag);
-  return cudaGetLastError();
+#define B200SHA3_CALL(R) alignment_check_for_rate<R>(offsets, lengths, count, unaligned_flag, stream)
+  B200SHA3_FOR_RATE(rate_bytes, B200SHA3_CALL)
+#undef B200SHA3_CALL
 }
 
 cudaError_t launch_generate_workload(uint64_t stream_seed, uint64_t message_size,
