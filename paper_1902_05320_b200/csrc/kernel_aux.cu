@@ -1,6 +1,8 @@
 // kernel_aux.cu -- everything around the hash kernels: device-side bucketing of
 // variable-length batches, the synthetic workload generators, and the raw
 // permutation test hook.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "keccak_f1600.cuh"
 
@@ -100,19 +102,24 @@ bucket_histogram_kernel(const uint64_t* __restrict__ offsets,
   __shared__ uint32_t local[kBucketBins];
   local[threadIdx.x] = 0u;
   __syncthreads();
-  const uint32_t base = blockIdx.x * (kBucketThreads * kBucketItems);
   const uint64_t len0 = lengths[0];
   const uint32_t first_tail = static_cast<uint32_t>(len0 - whole_blocks<RATE>(len0) * RATE);
   uint32_t misaligned = 0u, ragged = 0u, has_long = 0u;
+  // A block walks several tiles and flushes its counters once: the flush is one global atomic
+  // per bin and block, all blocks on the same few addresses.
+  constexpr uint32_t kTile = kBucketThreads * kBucketItems;
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kTile; base < count;
+       base += static_cast<uint64_t>(gridDim.x) * kTile) {
 #pragma unroll
-  for (int k = 0; k < kBucketItems; ++k) {
-    const uint32_t i = base + k * kBucketThreads + threadIdx.x;
-    if (i < count) {
-      const uint64_t len = lengths[i];
-      atomicAdd(&local[bucket_key<RATE>(len)], 1u);
-      misaligned |= static_cast<uint32_t>(offsets[i]) & 7u;
-      ragged |= static_cast<uint32_t>(len - whole_blocks<RATE>(len) * RATE) ^ first_tail;
-      has_long |= len >= RATE ? 1u : 0u;
+    for (int k = 0; k < kBucketItems; ++k) {
+      const uint64_t i = base + k * kBucketThreads + threadIdx.x;
+      if (i < count) {
+        const uint64_t len = lengths[i];
+        atomicAdd(&local[bucket_key<RATE>(len)], 1u);
+        misaligned |= static_cast<uint32_t>(offsets[i]) & 7u;
+        ragged |= static_cast<uint32_t>(len - whole_blocks<RATE>(len) * RATE) ^ first_tail;
+        has_long |= len >= RATE ? 1u : 0u;
+      }
     }
   }
   raise_flags(unaligned_flag, misaligned, ragged, has_long);
@@ -306,8 +313,8 @@ cudaError_t bucket_order_for_rate(const uint64_t* offsets, const uint64_t* lengt
   if (err != cudaSuccess) return err;
   const unsigned per_block = kBucketThreads * kBucketItems;
   const unsigned blocks = (count + per_block - 1) / per_block;
-  bucket_histogram_kernel<RATE><<<blocks, kBucketThreads, 0, stream>>>(offsets, lengths, count, hist,
-                                                                      unaligned_flag);
+  bucket_histogram_kernel<RATE><<<std::min(blocks, 148u * 8u), kBucketThreads, 0, stream>>>(offsets, lengths, count,
+                                                                                          hist, unaligned_flag);
   bucket_scan_kernel<<<1, kBucketBins, 0, stream>>>(hist, cursor);
   bucket_scatter_kernel<RATE><<<blocks, kBucketThreads, 0, stream>>>(
       lengths, count, hist, cursor, order, short_kernel_next ? unaligned_flag : nullptr);
