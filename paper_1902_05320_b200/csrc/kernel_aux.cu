@@ -44,10 +44,10 @@ __global__ void __launch_bounds__(128) permute_kernel(uint64_t* states, uint64_t
 // 2 x RL predicated ones (sponge.cuh: absorb_tail / absorb_tail_uniform_unaligned), which is
 // the difference between 0.90 and ~0.97 of the ALU roofline on short ragged batches.
 //
-// Key, 256 values, stored inverted so that key 0 is the heaviest bin:
+// Key, 512 values, stored inverted so that key 0 is the heaviest bin:
 //   one block    its word count len >> 2                      (0 .. 41)
-//   2 .. 63      42 + block count                              (44 .. 105)
-//   >= 64        16 sub-bins per power of two (<= 6.25 % spread inside a bin), clamped
+//   2 .. 128     40 + block count: every bin one block count   (42 .. 168)
+//   >= 129       16 sub-bins per power of two (<= 6.25 % spread inside a bin), clamped at 2^28 blocks
 // RATE is a template argument: the block count is a division by a compile-time constant
 // (multiply + shift) -- with a run-time divisor the two 64-bit divisions per message made
 // these passes compute bound (84 us for 2^24 messages against 45 us of memory traffic).
@@ -62,15 +62,15 @@ __device__ __forceinline__ uint32_t bucket_key(uint64_t len) {
   uint32_t key;
   if (blocks == 1u) {
     key = static_cast<uint32_t>(len) >> 2;  // < 42: the largest rate is 168 bytes
-  } else if (blocks < 64u) {
-    key = 42u + static_cast<uint32_t>(blocks);
+  } else if (blocks <= 128u) {
+    key = 40u + static_cast<uint32_t>(blocks);
   } else {
-    const int e = 63 - __clzll(static_cast<long long>(blocks));  // >= 6
+    const int e = 63 - __clzll(static_cast<long long>(blocks));  // >= 7
     const uint32_t frac = static_cast<uint32_t>(blocks >> (e - 4)) & 15u;
-    key = 106u + static_cast<uint32_t>(e - 6) * 16u + frac;
-    if (key > 255u) key = 255u;
+    key = 169u + static_cast<uint32_t>(e - 7) * 16u + frac;
+    if (key > kBucketBins - 1u) key = kBucketBins - 1u;
   }
-  return 255u - key;
+  return (kBucketBins - 1u) - key;
 }
 
 // Sets flags[0] / [1] / [2] if any thread of the warp saw a misaligned start / a different tail
@@ -88,8 +88,8 @@ __device__ __forceinline__ void raise_flags(uint32_t* flags, uint32_t misaligned
   }
 }
 
-constexpr int kBucketThreads = 256;
-constexpr int kBucketItems = 8;  // messages per thread
+constexpr int kBucketThreads = kBucketBins;
+constexpr int kBucketItems = 4;  // messages per thread
 static_assert(kBucketThreads == kBucketBins, "one thread per bin in the block-level steps");
 
 // scratch layout: [0,256) histogram / bin base, [256,512) running cursor,

@@ -103,7 +103,7 @@ cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream
 // launched after this pass) the order is left unwritten for a batch of single-block messages
 // with 8-byte aligned starts: that kernel takes those in input order.
 // `scratch` needs kBucketScratchWords 32-bit words.
-constexpr int kBucketBins = 256;
+constexpr int kBucketBins = 512;
 constexpr int kBucketScratchWords = 2 * kBucketBins + 8;
 cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,
                                 uint32_t count, uint32_t rate_bytes, uint32_t* order,

@@ -301,6 +301,7 @@ class Engine:
                                                         first_message, count, out.data_ptr(),
                                                         C.byref(cfg))
         self._check(rc)
+        self.total_kernel_launches += 1 if count else 0   # harness kernels count too (ncu sees them)
         return out[:count * message_size]
 
     def generate_lengths(self, count: int, min_len: int, max_len: int, *, seed_len: int = 2,
@@ -311,6 +312,7 @@ class Engine:
         rc = self.lib.b200sha3_generate_lengths_device(seed_len, min_len, max_len, first_message,
                                                        count, out.data_ptr(), C.byref(cfg))
         self._check(rc)
+        self.total_kernel_launches += 1 if count else 0
         return out[:count]
 
     def fill_messages(self, data, offsets, lengths, *, seed: int = 1, first_message: int = 0):
@@ -319,12 +321,14 @@ class Engine:
                                                     offsets.data_ptr(), lengths.data_ptr(),
                                                     data.data_ptr(), C.byref(cfg))
         self._check(rc)
+        self.total_kernel_launches += 1 if lengths.numel() else 0
 
     def permute_states(self, states):
         """In-place Keccak-f[1600] on a (n, 25) int64/uint64 CUDA tensor."""
         cfg, _, _ = self._config(self._torch_stream(), False)
         rc = self.lib.b200sha3_permute_device(states.data_ptr(), states.shape[0], C.byref(cfg))
         self._check(rc)
+        self.total_kernel_launches += 1 if states.shape[0] else 0
         return states
 
     def bucket_order(self, algorithm, lengths):

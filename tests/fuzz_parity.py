@@ -16,8 +16,8 @@ import torch  # noqa: E402
 
 from oracle.binding import Oracle  # noqa: E402
 from paper_1902_05320_b200 import BatchHasher, Engine  # noqa: E402
-from paper_1902_05320_b200.engine import (FLAG_NO_BUCKETING, FLAG_NO_PIPELINE, KERNEL_AUTO,  # noqa: E402
-                                          KERNEL_GENERIC, KERNEL_STAGED)
+from paper_1902_05320_b200.engine import (FLAG_NO_BUCKETING, FLAG_NO_PIPELINE, FLAG_NO_WARP_KERNEL,  # noqa: E402
+                                          KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STAGED, KERNEL_WARP)
 
 
 def random_lengths(rng, count, rate):
@@ -56,14 +56,17 @@ def main():
             pos += int(lengths[i])
         data = rng.integers(0, 256, pos + 16, dtype=np.uint8)
         expect = oracle.hash_batch(alg, data, offsets, lengths, xof_bits=bits, workers=8)
-        entry = str(rng.choice(["device", "device_nobucket", "device_staged", "host", "host_nopipe",
+        entry = str(rng.choice(["device", "device_nobucket", "device_staged", "device_warp", "host", "host_nopipe",
                                 "fixed_device", "fixed_host", "incremental"]))
+        # small batches take the warp-per-state kernel by default: half of the cases switch it off
+        # so that the one-message-per-thread kernels see small batches too
+        no_warp = FLAG_NO_WARP_KERNEL if rng.random() < 0.5 else 0
         if entry.startswith("fixed"):
             n = int(lengths[0])
             fixed = rng.integers(0, 256, max(count * n, 1) + 16, dtype=np.uint8)
             expect = oracle.hash_batch(alg, fixed, fixed_len=n, count=count, xof_bits=bits, workers=8)
-            kernel = int(rng.choice([KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STAGED]))
-            eng = Engine(kernel=kernel)
+            kernel = int(rng.choice([KERNEL_AUTO, KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STAGED, KERNEL_WARP]))
+            eng = Engine(kernel=kernel, flags=no_warp)
             if entry == "fixed_device":
                 got = eng.hash_fixed(alg, torch.from_numpy(fixed).cuda(), n, count, bits).cpu().numpy()
             else:
@@ -78,13 +81,13 @@ def main():
             got = (h.digest() if alg < 4 else h.finish(bits)).cpu().numpy()
             h.close()
         elif entry.startswith("device"):
-            flags = FLAG_NO_BUCKETING if entry == "device_nobucket" else 0
-            kernel = KERNEL_STAGED if entry == "device_staged" else KERNEL_AUTO
+            flags = (FLAG_NO_BUCKETING if entry == "device_nobucket" else 0) | no_warp
+            kernel = {"device_staged": KERNEL_STAGED, "device_warp": KERNEL_WARP}.get(entry, KERNEL_AUTO)
             eng = Engine(flags=flags, kernel=kernel)
             got = eng.hash_batch(alg, torch.from_numpy(data).cuda(), torch.from_numpy(offsets.astype(np.int64)).cuda(),
                                  torch.from_numpy(lengths.astype(np.int64)).cuda(), bits).cpu().numpy()
         else:
-            eng = Engine(flags=FLAG_NO_PIPELINE if entry == "host_nopipe" else 0)
+            eng = Engine(flags=(FLAG_NO_PIPELINE if entry == "host_nopipe" else 0) | no_warp)
             got = eng.hash_batch(alg, data, offsets, lengths, bits)
         if not (got == expect).all():
             bad = int(np.argwhere((got != expect).any(axis=1))[0][0])

@@ -309,7 +309,7 @@ def test_staged_kernel(oracle, algorithm):
 
 def test_bucket_order_is_a_sorted_permutation(big_engine):
     """Device bucketing: every index exactly once; keys non-increasing, the key being the block
-    count below 64 blocks, 16 sub-bins per power of two above, and -- among single-block
+    count up to 128 blocks, 16 sub-bins per power of two above, and -- among single-block
     messages -- the number of whole 32-bit words (kernel_aux.cu: bucket_key)."""
     engine = big_engine
     import torch
@@ -317,10 +317,10 @@ def test_bucket_order_is_a_sorted_permutation(big_engine):
     def key(lengths):
         blocks = lengths // 136 + 1
         e = np.floor(np.log2(np.maximum(blocks, 1))).astype(np.int64)
-        coarse = 106 + (e - 6) * 16 + ((blocks >> np.maximum(e - 4, 0)) & 15)
-        return np.where(blocks == 1, lengths >> 2, np.where(blocks < 64, 42 + blocks, np.minimum(coarse, 255)))
+        coarse = 169 + (e - 7) * 16 + ((blocks >> np.maximum(e - 4, 0)) & 15)
+        return np.where(blocks == 1, lengths >> 2, np.where(blocks <= 128, 40 + blocks, np.minimum(coarse, 511)))
 
-    for lo, hi in ((1, 16384), (0, 135), (0, 400)):
+    for lo, hi in ((1, 16384), (0, 135), (0, 400), (1, 200_000)):
         lengths = engine.generate_lengths(200_000, lo, hi, seed_len=2)
         order = engine.bucket_order("sha3_256", lengths).cpu().numpy().astype(np.int64)
         assert np.array_equal(np.sort(order), np.arange(200_000))
@@ -328,7 +328,9 @@ def test_bucket_order_is_a_sorted_permutation(big_engine):
         keys = key(host)[order]
         assert (np.diff(keys) <= 0).all()
         blocks = (host // 136 + 1)[order]
-        assert blocks[0] >= blocks.max() - 3 and blocks[-1] == blocks.min()   # 64..127 blocks: bins of 4
+        assert blocks[0] >= blocks.max() * 15 // 16 and blocks[-1] == blocks.min()
+        if hi <= 16384:
+            assert (np.diff(blocks) <= 0).all()      # up to 128 blocks every bin is one block count
     torch.cuda.synchronize()
 
 
