@@ -22,10 +22,14 @@ constexpr int kDefaultUnrollOneblock = 23;  // peeled 1 + 7x3 + 2 (17 KB): 4.43 
 constexpr int kDefaultFmaOneblock = 0;
 constexpr int kDefaultFmaGeneric = 0;
 
+}  // namespace
+
+char* last_error_buffer() { return g_last_error; }
+
 // Batches of at most this many messages go to the warp-per-state kernel (kernel_warp.cu) when
-// they are multi-block: one warp per message then finishes a permutation in a quarter of the
-// time one thread needs, and the machine has warps to spare (592 SMSPs).  Above it the
-// shuffle unit saturates and one message per thread is faster again (DESIGN.md section 4,
+// they are multi-block: one warp per message then finishes a permutation in 0.4x the time one
+// thread needs, and the machine has warps to spare (592 SMSPs).  Above it the shuffle unit
+// saturates and one message per thread is faster again (DESIGN.md section 3.3c,
 // tools/long_message_latency.py).  B200SHA3_WARP_KERNEL_MAX overrides it for experiments.
 uint64_t warp_kernel_max_count() {
   static const uint64_t value = [] {
@@ -34,9 +38,6 @@ uint64_t warp_kernel_max_count() {
   }();
   return value;
 }
-}  // namespace
-
-char* last_error_buffer() { return g_last_error; }
 
 namespace {
 class SideLaneCache {

@@ -163,6 +163,13 @@ struct SideLane {
 };
 cudaError_t side_lane(SideLane* out);
 
+// Largest batch (messages / streams) KERNEL_AUTO gives to the warp-per-state kernels.
+uint64_t warp_kernel_max_count();
+inline bool few_enough_for_warps(uint64_t count, const Config& c) {
+  return count <= warp_kernel_max_count() && (c.flags & B200SHA3_FLAG_NO_WARP_KERNEL) == 0 &&
+         (c.kernel == B200SHA3_KERNEL_AUTO || c.kernel == B200SHA3_KERNEL_WARP);
+}
+
 // Keeps stream-ordered allocations cached between calls (once per process).
 void tune_mempool_once();
 

@@ -146,8 +146,10 @@ static int states_update(b200sha3_states* st, const uint8_t* d_data, const uint6
   const Config c = resolve(cfg);
   DeviceGuard guard;
   CU(guard.enter(st->device));
-  CU(launch_states_update(kVariants[st->algorithm].rate_lanes, st->lanes, st->pos, st->count,
-                          d_data, d_offsets, d_lengths, fixed_len, c.stream));
+  // few streams: one warp each (kernel_stream_warp.cu); the state layout is the same
+  CU((few_enough_for_warps(st->count, c) ? launch_states_update_warp : launch_states_update)(
+      kVariants[st->algorithm].rate_lanes, st->lanes, st->pos, st->count, d_data, d_offsets, d_lengths,
+      fixed_len, c.stream));
   if (c.kernel_launches) *c.kernel_launches = 1;
   return B200SHA3_OK;
 }
@@ -174,8 +176,9 @@ int b200sha3_states_finish_device(b200sha3_states* st, uint64_t xof_output_bits,
   const Config c = resolve(cfg);
   DeviceGuard guard;
   CU(guard.enter(st->device));
-  CU(launch_states_finish(v.rate_lanes, st->lanes, st->pos, st->count, v.head, d_digests, out_len,
-                          last_byte_mask(st->algorithm, xof_output_bits), c.stream));
+  CU((few_enough_for_warps(st->count, c) ? launch_states_finish_warp : launch_states_finish)(
+      v.rate_lanes, st->lanes, st->pos, st->count, v.head, d_digests, out_len,
+      last_byte_mask(st->algorithm, xof_output_bits), c.stream));
   st->finished = true;
   if (c.kernel_launches) *c.kernel_launches = st->count ? 1 : 0;
   return B200SHA3_OK;
@@ -191,8 +194,8 @@ int b200sha3_states_squeeze_device(b200sha3_states* st, uint64_t out_bytes, uint
   const Config c = resolve(cfg);
   DeviceGuard guard;
   CU(guard.enter(st->device));
-  CU(launch_states_squeeze(kVariants[st->algorithm].rate_lanes, st->lanes, st->pos, st->count,
-                           d_out, out_bytes, c.stream));
+  CU((few_enough_for_warps(st->count, c) ? launch_states_squeeze_warp : launch_states_squeeze)(
+      kVariants[st->algorithm].rate_lanes, st->lanes, st->pos, st->count, d_out, out_bytes, c.stream));
   if (c.kernel_launches) *c.kernel_launches = 1;
   return B200SHA3_OK;
 }

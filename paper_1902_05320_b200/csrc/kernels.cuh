@@ -135,6 +135,17 @@ cudaError_t launch_states_finish(int rate_lanes, void* lanes, uint32_t* pos, uin
 cudaError_t launch_states_squeeze(int rate_lanes, void* lanes, uint32_t* pos, uint64_t count,
                                   uint8_t* out, uint64_t out_len, cudaStream_t stream);
 
+// The same three steps with one stream per WARP (kernel_stream_warp.cu): same state layout, for
+// few streams.
+cudaError_t launch_states_update_warp(int rate_lanes, void* lanes, uint32_t* pos, uint64_t count,
+                                      const uint8_t* data, const uint64_t* offsets,
+                                      const uint64_t* lengths, uint64_t fixed_len, cudaStream_t stream);
+cudaError_t launch_states_finish_warp(int rate_lanes, void* lanes, uint32_t* pos, uint64_t count,
+                                      uint32_t head, uint8_t* out, uint64_t out_len, uint32_t last_mask,
+                                      cudaStream_t stream);
+cudaError_t launch_states_squeeze_warp(int rate_lanes, void* lanes, uint32_t* pos, uint64_t count,
+                                       uint8_t* out, uint64_t out_len, cudaStream_t stream);
+
 // Pipe microbenchmark; see b200sha3_probe_pipe.
 cudaError_t run_pipe_probe(int mix, double* instr_per_s, double* sm_hz, cudaStream_t stream);
 

@@ -730,3 +730,44 @@ def test_long_messages_are_cut_into_chunks_by_bytes(big_engine):
     dev = engine.hash_batch("sha3_256", torch.from_numpy(blob).cuda(), torch.from_numpy(offsets.view(np.int64)).cuda(),
                             torch.from_numpy(lengths.view(np.int64)).cuda())
     assert (dev.cpu().numpy() == got).all()
+
+
+def test_device_entries_can_be_captured_in_a_cuda_graph(oracle):
+    """The device-buffer entries only enqueue work (kernels, stream-ordered scratch, an event
+    fork / join for the two alternative kernels of a variable-length batch), so a caller can
+    capture them in a CUDA graph and replay it on new data in the same buffers."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_WARP_KERNEL
+    eng = Engine(flags=FLAG_NO_WARP_KERNEL)      # the multi-launch path: bucketing + both hash kernels
+    rng = np.random.default_rng(5)
+    count = 3000
+    lengths = rng.integers(0, 130, count).astype(np.uint64)
+    offsets = np.concatenate([[0], np.cumsum(lengths)[:-1]]).astype(np.uint64)
+    blob = rng.integers(0, 256, int(lengths.sum()) + 16, dtype=np.uint8)
+    d, o, l = to_device(blob, offsets, lengths)
+    fixed = torch.from_numpy(rng.integers(0, 256, 4096 * 64, dtype=np.uint8)).cuda()
+    out_var = torch.empty((count, 32), dtype=torch.uint8, device="cuda")
+    out_fix = torch.empty((4096, 32), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):              # warm-up outside the capture (pools, side lane)
+        eng.hash_batch("sha3_256", d, o, l, out=out_var)
+        eng.hash_fixed("sha3_256", fixed, 64, 4096, out=out_fix)
+    torch.cuda.current_stream().wait_stream(stream)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        eng.hash_batch("sha3_256", d, o, l, out=out_var)
+        eng.hash_fixed("sha3_256", fixed, 64, 4096, out=out_fix)
+    for trial in range(3):                       # new bytes in the same buffers, replay
+        blob2 = rng.integers(0, 256, blob.size, dtype=np.uint8)
+        fixed2 = rng.integers(0, 256, 4096 * 64, dtype=np.uint8)
+        d.copy_(torch.from_numpy(blob2))
+        fixed.copy_(torch.from_numpy(fixed2))
+        out_var.zero_()
+        out_fix.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert (out_var.cpu().numpy() == oracle.hash_batch(1, blob2, offsets, lengths, workers=4)).all()
+        assert (out_fix.cpu().numpy() == oracle.hash_batch(1, fixed2, fixed_len=64, count=4096, workers=4)).all()

@@ -11,6 +11,18 @@ pytestmark = pytest.mark.gpu
 HASHLIB = ["sha3_224", "sha3_256", "sha3_384", "sha3_512", "shake_128", "shake_256"]
 
 
+@pytest.fixture(scope="module", params=["auto", "no_warp_kernel"])
+def engine(request):
+    """Every test runs on both forms of the incremental kernels: one stream per warp (what
+    KERNEL_AUTO picks for the few hundred streams used here) and one stream per thread."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test selected but no CUDA device is visible")
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_WARP_KERNEL
+    return Engine(flags=FLAG_NO_WARP_KERNEL if request.param == "no_warp_kernel" else 0)
+
+
 def feed(hasher, messages, cuts, rng):
     """Feeds message i in pieces ending at cuts[i][k]; round k sends piece k of every stream
     (zero-length where a stream has fewer pieces), packed at random byte offsets."""
@@ -134,3 +146,40 @@ def test_one_long_stream_in_pieces(engine):
         h.update(torch.from_numpy(piece.copy()).cuda(), chunk_len=n)
         pos += n
     assert h.digest().cpu().numpy()[0].tobytes() == ref.digest()
+
+
+@pytest.mark.parametrize("algorithm", [1, 3, 4])
+def test_warp_and_thread_forms_share_the_states(oracle, algorithm):
+    """The two forms of the incremental kernels keep the same state layout in HBM: updates may
+    alternate between them on one set of states, and either may finish / squeeze."""
+    import torch
+    from paper_1902_05320_b200 import BatchHasher, Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_WARP_KERNEL
+    rng = np.random.default_rng(90 + algorithm)
+    rate = oracle.rate_bytes(algorithm)
+    n = 300
+    engines = [Engine(), Engine(flags=FLAG_NO_WARP_KERNEL)]
+    messages = [rng.integers(0, 256, int(L), dtype=np.uint8).tobytes() for L in rng.integers(0, 6 * rate, n)]
+    h = BatchHasher(algorithm, n, engines[0])
+    done = [0] * n
+    for step in range(5):                       # five rounds of pieces, alternating the form
+        h.engine = engines[step % 2]
+        take = [int(rng.integers(0, len(m) - d + 1)) if step < 4 else len(m) - d for m, d in zip(messages, done)]
+        lengths = np.array(take, dtype=np.int64)
+        offsets = np.concatenate([[0], np.cumsum(lengths)[:-1]]).astype(np.int64)
+        blob = b"".join(m[d:d + k] for m, d, k in zip(messages, done, take)) + b"\0" * 8
+        h.update(torch.from_numpy(np.frombuffer(blob, dtype=np.uint8).copy()).cuda(),
+                 torch.from_numpy(offsets).cuda(), torch.from_numpy(lengths).cuda())
+        done = [d + k for d, k in zip(done, take)]
+    if algorithm < 4:
+        got = h.digest().cpu().numpy()
+        want = [oracle.hash_one(algorithm, m) for m in messages]
+    else:
+        h.engine = engines[1]
+        first = h.finish(8 * 100).cpu().numpy()                      # 100 bytes by the thread form ...
+        h.engine = engines[0]
+        more = h.read(2 * rate + 7).cpu().numpy()                    # ... the rest by the warp form
+        got = np.concatenate([first, more], axis=1)
+        want = [oracle.hash_one(algorithm, m, 8 * (100 + 2 * rate + 7)) for m in messages]
+    assert [g.tobytes() for g in got] == want
+    h.close()
