@@ -97,9 +97,12 @@ enum {
   B200SHA3_KERNEL_STAGED = 4,    /* generic kernel with rate blocks staged through
                                     shared memory by bulk async copies (TMA); also
                                     kept for the measured comparison               */
-  B200SHA3_KERNEL_WARP = 5       /* one message per warp (25 lanes over 25 threads,
+  B200SHA3_KERNEL_WARP = 5,      /* one message per warp (25 lanes over 25 threads,
                                     shuffles): AUTO picks it for batches of few
                                     multi-block messages                           */
+  B200SHA3_KERNEL_PAIR = 6       /* one message per pair of threads (low / high halves
+                                    of every lane, one shuffle per rotation): kept
+                                    for the measured comparison, never AUTO         */
 };
 
 /* Optional per-call configuration; NULL means all defaults.  The analogue of

@@ -144,6 +144,8 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
   cudaError_t err;
   if (kernel == B200SHA3_KERNEL_WARP) {
     err = launch_hash_warp(args, plan, stream);
+  } else if (kernel == B200SHA3_KERNEL_PAIR) {
+    err = launch_hash_pair(args, plan, stream);
   } else if (fits_short) {
     err = launch_hash_short_fixed(args, plan, stream);
   } else if (kernel == B200SHA3_KERNEL_ONEBLOCK) {
@@ -305,6 +307,7 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
       if (err == cudaSuccess && launches) *launches += 1;
     } else {
       err = c.kernel == B200SHA3_KERNEL_STAGED ? launch_hash_staged(args, plan, stream)
+            : c.kernel == B200SHA3_KERNEL_PAIR ? launch_hash_pair(args, plan, stream)
                                                : launch_hash_generic(args, plan, stream);
       if (err == cudaSuccess && launches) *launches += 1;
     }

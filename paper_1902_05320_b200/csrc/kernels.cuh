@@ -88,6 +88,12 @@ bool lanesplit_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes
 // size; args.order may be nullptr.
 cudaError_t launch_hash_warp(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
 
+// Pair-split kernel (kernel_pair.cu): one message per PAIR of threads (low / high 32-bit halves
+// of every lane, one shuffle per rotation).  A measured experiment (no faster than one message
+// per thread: the shuffles cost the issue slots the halved ALU work frees); forced selection
+// only.  Honours order / skip_if_short like the generic kernel.
+cudaError_t launch_hash_pair(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
+
 // TMA-staged variant of the generic kernel (kernel_staged.cu); blocks are staged when the
 // data base is 16-byte aligned and message starts are 8-byte aligned (else direct loads).
 cudaError_t launch_hash_staged(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);

@@ -113,3 +113,30 @@ def test_empty_messages_and_one_message(warp_engine, oracle):
         assert [r.tobytes() for r in got] == [oracle.hash_one(algorithm, m, bits) for m in msgs]
         got = device_digests(warp_engine, algorithm, [b"abc"], bits)
         assert got[0].tobytes() == oracle.hash_one(algorithm, b"abc", bits)
+
+
+@pytest.mark.parametrize("path", all_kat_files()[::3], ids=lambda p: p.stem)
+def test_pair_split_kernel(oracle, path):
+    """The pair-split comparison kernel (csrc/kernel_pair.cu: low / high halves of every lane in
+    two threads, one shuffle per rotation) gives the same digests: reference vectors at odd and
+    aligned packings, multi-block messages with an odd XOF bit count, equal-length entry."""
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import KERNEL_PAIR
+    eng = Engine(kernel=KERNEL_PAIR)
+    algorithm, out_bits, vectors = load_kat_file(path)
+    bits = xof_bits_for(algorithm, out_bits)
+    msgs = [m for m, _ in vectors]
+    for align, lead in ((1, 3), (4, 0), (8, 0)):
+        got = device_digests(eng, algorithm, msgs, bits, align, lead)
+        for row, (_, md) in zip(got, vectors):
+            assert row.tobytes() == md
+    rate = oracle.rate_bytes(algorithm)
+    bits = 17 * rate + 3 if algorithm >= 4 else 0
+    rng = np.random.default_rng(algorithm)
+    msgs = [rng.integers(0, 256, int(n), dtype=np.uint8).tobytes() for n in rng.integers(0, 9 * rate, 777)]
+    got = device_digests(eng, algorithm, msgs, bits)
+    assert [r.tobytes() for r in got] == [oracle.hash_one(algorithm, m, bits) for m in msgs]
+    host = oracle.generate_workload(3001 * 500, 500, seed=2)
+    want = oracle.hash_batch(algorithm, host, fixed_len=500, count=3001, xof_bits=bits, workers=8)
+    assert (eng.hash_fixed(algorithm, torch.from_numpy(host).cuda(), 500, 3001, bits).cpu().numpy() == want).all()
