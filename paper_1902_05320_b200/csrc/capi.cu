@@ -297,10 +297,14 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
       err = side_lane(&side);
       if (err == cudaSuccess) err = cudaEventRecord(side.fork, stream);
       if (err == cudaSuccess) err = cudaStreamWaitEvent(side.stream, side.fork, 0);
-      if (err == cudaSuccess) err = launch_hash_generic(args, plan, side.stream);
-      if (err == cudaSuccess) err = launch_hash_short(args, plan, stream);
-      if (err == cudaSuccess) err = cudaEventRecord(side.join, side.stream);
-      if (err == cudaSuccess) err = cudaStreamWaitEvent(stream, side.join, 0);
+      if (err == cudaSuccess) {
+        err = launch_hash_generic(args, plan, side.stream);
+        if (err == cudaSuccess) err = launch_hash_short(args, plan, stream);
+        // join whatever happened: the scratch is freed in `stream` order
+        cudaError_t joined = cudaEventRecord(side.join, side.stream);
+        if (joined == cudaSuccess) joined = cudaStreamWaitEvent(stream, side.join, 0);
+        if (err == cudaSuccess) err = joined;
+      }
       if (err == cudaSuccess && launches) *launches += 2;
     } else if (host_short) {
       err = launch_hash_short(args, plan, stream);
