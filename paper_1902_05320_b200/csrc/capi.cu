@@ -39,39 +39,6 @@ uint64_t warp_kernel_max_count() {
   return value;
 }
 
-namespace {
-class SideLaneCache {
- public:
-  cudaError_t get(SideLane* out) {
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    if (dev >= static_cast<int>(lanes_.size())) lanes_.resize(dev + 1);
-    SideLane& lane = lanes_[dev];
-    if (!lane.stream) {
-      e = cudaStreamCreateWithFlags(&lane.stream, cudaStreamNonBlocking);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&lane.fork, cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&lane.join, cudaEventDisableTiming);
-      if (e != cudaSuccess) return e;
-    }
-    *out = lane;
-    return cudaSuccess;
-  }
-  ~SideLaneCache() {
-    for (SideLane& lane : lanes_) {  // harmless errors if the context is already gone
-      if (lane.fork) cudaEventDestroy(lane.fork);
-      if (lane.join) cudaEventDestroy(lane.join);
-      if (lane.stream) cudaStreamDestroy(lane.stream);
-    }
-  }
-
- private:
-  std::vector<SideLane> lanes_;
-};
-thread_local SideLaneCache t_side_lanes;
-}  // namespace
-
-cudaError_t side_lane(SideLane* out) { return t_side_lanes.get(out); }
 
 void tune_mempool_once() {
   static std::once_flag once;
@@ -250,9 +217,9 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     uint32_t* bucket_scratch = scratch + 8;
     uint32_t* order = bucketing ? scratch + 8 + kBucketScratchWords : nullptr;
     CU(cudaMemsetAsync(flag, 0, 8 * sizeof(uint32_t), stream));
-    // Batches of single-block messages only have their own kernel (kernel_short.cu).  Without
-    // host knowledge, whether this is one is known on the device only (flag words), so both
-    // kernels are launched and one of them returns at once.
+    // Batches of single-block messages only have their own kernel body (kernel_short.cu).  Without
+    // host knowledge, whether this is one is known on the device only (flag words): the merged
+    // kernel of kernel_ragged.cu carries both bodies and branches on the flag.
     const bool try_short = hints ? host_short : short_shape;
     if (host_short) {  // "nothing long" (word 2 stays zero); word 0 says whether the starts are aligned
       if (!hints->aligned8) CU(cudaMemsetAsync(flag, 1, sizeof(uint32_t), stream));
@@ -275,7 +242,7 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     args.unaligned_flag = is_aligned(d_data, 8) ? flag : nullptr;
     args.ragged_flag = flag + 1;
     args.long_flag = flag + 2;
-    args.skip_if_short = (try_short && !host_short) ? 1u : 0u;
+    args.skip_if_short = 0u;
     args.aligned8 = 0u;  // used only when the base pointer itself is misaligned
     args.digests = d_digests + first * digest_bytes;
     args.digest_bytes = digest_bytes;
@@ -288,24 +255,11 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     plan.block_threads = c.block_threads;
     cudaError_t err = cudaSuccess;
     if (try_short && !host_short) {
-      // Two alternatives, decided by the flag words on the device: one of the two kernels
-      // returns at once -- 131072 empty blocks for 2^24 messages, 70 us in line.  Launched side
-      // by side (the generic kernel on the side lane, first), the empty one drains while the
-      // other starts.  (Halving the empty grid with 256-thread blocks for the generic kernel was
-      // measured: nothing gained when it is the empty one, 7 % lost when it is the real one.)
-      SideLane side;
-      err = side_lane(&side);
-      if (err == cudaSuccess) err = cudaEventRecord(side.fork, stream);
-      if (err == cudaSuccess) err = cudaStreamWaitEvent(side.stream, side.fork, 0);
-      if (err == cudaSuccess) {
-        err = launch_hash_generic(args, plan, side.stream);
-        if (err == cudaSuccess) err = launch_hash_short(args, plan, stream);
-        // join whatever happened: the scratch is freed in `stream` order
-        cudaError_t joined = cudaEventRecord(side.join, side.stream);
-        if (joined == cudaSuccess) joined = cudaStreamWaitEvent(stream, side.join, 0);
-        if (err == cudaSuccess) err = joined;
-      }
-      if (err == cudaSuccess && launches) *launches += 2;
+      // Short or generic, decided by the flag words on the device: one launch with both bodies
+      // (kernel_ragged.cu).  Launching both kernels and letting one return at once cost the
+      // dispatch of its whole grid -- 70 us for 2^24 messages, side by side or not.
+      err = launch_hash_ragged(args, plan, stream);
+      if (err == cudaSuccess && launches) *launches += 1;
     } else if (host_short) {
       err = launch_hash_short(args, plan, stream);
       if (err == cudaSuccess && launches) *launches += 1;

@@ -154,15 +154,6 @@ class AsyncScratch {
   cudaStream_t stream_ = nullptr;
 };
 
-// A second stream (plus the two events of a fork / join) next to the caller's, cached per calling
-// thread and device: run_batch_device launches the two alternative hash kernels of a
-// variable-length batch side by side, so that the one that returns at once costs nothing.
-struct SideLane {
-  cudaStream_t stream = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-cudaError_t side_lane(SideLane* out);
-
 // Largest batch (messages / streams) KERNEL_AUTO gives to the warp-per-state kernels.
 uint64_t warp_kernel_max_count();
 inline bool few_enough_for_warps(uint64_t count, const Config& c) {

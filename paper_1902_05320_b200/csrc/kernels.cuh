@@ -21,8 +21,9 @@ struct HashArgs {
                                    // batch differ in length; nullptr: they are all alike
   const uint32_t* long_flag;       // device word, nonzero if some message fills a whole rate block
                                    // (>= rate bytes); nullptr: unknown
-  uint32_t skip_if_short;          // generic kernel: leave the batch to hash_short_kernel when it
-                                   // is all-short (the flag above says so)
+  uint32_t skip_if_short;          // generic / pair kernel: return at once when the batch is
+                                   // all-short (the flag above says so); for callers that launch
+                                   // hash_short_kernel next to it (none does by default)
   uint8_t* digests;          // count * digest_bytes, message order
   uint64_t digest_bytes;
   uint32_t head;             // pad head byte: 0x06 / 0x1f
@@ -75,6 +76,11 @@ cudaError_t launch_hash_short(const HashArgs& args, const LaunchPlan& plan, cuda
 bool short_supported(int rate_lanes, uint64_t digest_bytes);
 // Equal-length form: any length below the rate (args.fixed_len), any alignment (args.aligned8).
 cudaError_t launch_hash_short_fixed(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
+
+// One launch for a variable-length batch classified on the device (kernel_ragged.cu): the short
+// kernel's body if the flag words say "nothing as long as the rate", the generic kernel's body
+// otherwise.  Same shapes as short_supported; cudaErrorNotSupported otherwise.
+cudaError_t launch_hash_ragged(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
 
 // Lane-split kernel (5 threads per state, warp shuffles); equal-length,
 // 8-byte aligned, single-block messages.
