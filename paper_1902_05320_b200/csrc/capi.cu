@@ -310,9 +310,12 @@ const char* b200sha3_selected_kernel(int algorithm, uint64_t msg_len, uint64_t c
   if (few && (msg_len == UINT64_MAX || b200sha3_permutations(algorithm, msg_len, xof_output_bits) >= 2)) {
     std::snprintf(name, sizeof name, "hash_warp_kernel");  // run_fixed_slice / run_batch_device
   } else if (msg_len == UINT64_MAX) {  // run_batch_device: classification on the device
-    std::snprintf(name, sizeof name, "bucket_order + %shash_generic_kernel<%d>",
-                  whole_bytes && short_supported(v.rate_lanes, digest_bytes) ? "hash_short_kernel | " : "",
-                  v.rate_lanes);
+    if (whole_bytes && short_supported(v.rate_lanes, digest_bytes)) {
+      std::snprintf(name, sizeof name, "bucket_order + hash_ragged_kernel<%d,%d>", v.rate_lanes,
+                    static_cast<int>(digest_bytes / 4));
+    } else {
+      std::snprintf(name, sizeof name, "bucket_order + hash_generic_kernel<%d>", v.rate_lanes);
+    }
   } else if (whole_bytes && oneblock_supported(v.rate_lanes, msg_len, digest_bytes)) {  // run_fixed_slice
     std::snprintf(name, sizeof name, "hash_oneblock_kernel<%d,%d,%d>", v.rate_lanes,
                   static_cast<int>(msg_len / 8), static_cast<int>(digest_bytes / 4));

@@ -158,8 +158,8 @@ def test_selected_kernel_names():
     assert selected_kernel("sha3_512", 1024) == "hash_generic_kernel<9>"
     assert selected_kernel("shake128", 64, 1023) == "hash_generic_kernel<21>"     # odd bits: masked tail
     assert selected_kernel("shake128", 64, 1024) == "hash_oneblock_kernel<21,8,32>"
-    assert "hash_short_kernel" in selected_kernel("sha3_256", None)
-    assert "hash_short_kernel" not in selected_kernel("shake256", None, 4099)
+    assert selected_kernel("sha3_256", None) == "bucket_order + hash_ragged_kernel<17,8>"
+    assert selected_kernel("shake256", None, 4099) == "bucket_order + hash_generic_kernel<17>"
     assert selected_kernel(9, 64) == ""
     # few multi-block messages: one warp per message
     assert selected_kernel("sha3_256", 1 << 20, count=1024) == "hash_warp_kernel"
