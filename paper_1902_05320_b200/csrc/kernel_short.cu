@@ -4,13 +4,10 @@
 // The generic kernel serves such a batch at ~0.93 of the ALU roofline and ncu shows why: no
 // stalls, just instructions -- a rolled permutation that cannot drop the work on the capacity
 // lanes (zero before the first permutation) or on the lanes nobody reads after the last one,
-// the block-count loop, the processing order.  When the classification pass
-// (kernel_aux.cu) finds no message of a whole block, this kernel does the batch instead
-// (8-byte aligned starts: 8-byte loads; any other layout: aligned 4-byte loads + PRMT): lane
-// loads straight into a zero state, the peeled permutation of the one-block kernel
-// (1 + 7x3 + 2 rounds), OW digest words out; messages taken in the order of the bucketing pass
-// (by word count) when there is one, else in input order.  It is launched next to the
-// generic kernel; each of the two returns at once when the flags give the batch to the other.
+// the block-count loop, the processing order.  For batches without a message of a whole block
+// the kernels here do the work instead (8-byte aligned starts: 8-byte loads; any other layout:
+// aligned 4-byte loads + PRMT): lane loads straight into a zero state, the peeled permutation
+// of the one-block kernel (1 + 7x3 + 2 rounds), OW digest words out.
 #include "kernels.cuh"
 #include "sponge.cuh"
 
@@ -18,17 +15,17 @@ namespace b200sha3 {
 
 namespace {
 
-// The final block is absorbed by the predicated "ragged" form (~6 ALU instructions per lane on
-// 8-byte aligned starts: 0.97 of the roofline in input order).  Starts at odd addresses cost
-// ~10 per lane that way (0.90), so for those -- SORTED -- args.order lists the messages by
-// their number of whole 32-bit words (the bucketing pass, kernel_aux.cu): the threads of a
-// warp then hold final blocks of the same shape (all but the warps that straddle two bins) and
-// the jump table of statically indexed 4-byte loads + PRMT applies (0.94 including the pass).
-template <int RL, int OW, bool SORTED>
+// Input order, predicated "ragged" absorb (~6 ALU instructions per lane on 8-byte aligned
+// starts, ~10 per lane on 4-byte loads + PRMT otherwise).  Launched by the host entries, which
+// know from the lengths they read that the batch is all-short (BatchHints) and run no
+// classification or ordering pass; the device entries use hash_ragged_kernel (kernel_ragged.cu),
+// which carries this body -- plus the word-count-ordered jump-table form for batches at odd
+// addresses -- next to the generic one.
+template <int RL, int OW>
 __global__ void __launch_bounds__(256)
 hash_short_kernel(const HashArgs args) {
   static_assert(OW <= 2 * RL, "digest must fit one block");
-  if (*args.long_flag != 0u) return;  // the generic kernel's batch
+  if (*args.long_flag != 0u) return;  // not an all-short batch: nothing to do here
   const bool aligned8 = *args.unaligned_flag == 0u;  // else: 4-byte loads re-assembled with PRMT
   // (A persistent grid-stride form of this kernel was measured 4 % slower on its own batches:
   // 0.921 vs 0.957 of the roofline on 2^24 x 0..135 B.  So was a tile form -- a block
@@ -36,19 +33,13 @@ hash_short_kernel(const HashArgs args) {
   // tile, no ordering pass, no far gathers: 0.921 aligned / 0.891 unaligned on the same batch.)
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (tid >= args.count) return;
-  const bool sorted = SORTED && !aligned8;  // (the bucketing pass writes no order for aligned batches)
-  const uint64_t m = sorted ? static_cast<uint64_t>(args.order[tid]) : tid;
-  const uint8_t* p = args.data + args.offsets[m];
-  const uint32_t len = static_cast<uint32_t>(args.lengths[m]);  // < 8 * RL
+  const uint8_t* p = args.data + args.offsets[tid];
+  const uint32_t len = static_cast<uint32_t>(args.lengths[tid]);  // < 8 * RL
   State a;
   state_zero(a);
-  if (sorted) {
-    absorb_tail_uniform_unaligned<RL>(a, p, len, args.head);
-  } else {
-    absorb_tail<RL>(a, p, len, args.head, aligned8, /*ragged=*/true);
-  }
+  absorb_tail<RL>(a, p, len, args.head, aligned8, /*ragged=*/true);
   keccak_f1600<23, 0u>(a);  // peeled 1 + 7x3 + 2
-  emit_block<RL>(a, args.digests + m * (4u * OW), 4u * OW);
+  emit_block<RL>(a, args.digests + tid * (4u * OW), 4u * OW);
 }
 
 // The same for EQUAL-LENGTH batches of any length below the rate -- what the one-block kernel
@@ -92,11 +83,7 @@ cudaError_t launch_instance(const HashArgs& args, const LaunchPlan& plan, cudaSt
   const uint64_t blocks = (args.count + threads - 1) / threads;
   if (blocks == 0) return cudaSuccess;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
-  if (args.order) {
-    hash_short_kernel<RL, OW, true><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(args);
-  } else {
-    hash_short_kernel<RL, OW, false><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(args);
-  }
+  hash_short_kernel<RL, OW><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(args);
   return cudaGetLastError();
 }
 
@@ -131,7 +118,7 @@ cudaError_t launch_hash_short_fixed(const HashArgs& args, const LaunchPlan& plan
 
 cudaError_t launch_hash_short(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {
   if (!short_supported(plan.rate_lanes, args.digest_bytes) || !args.offsets || !args.lengths ||
-      !args.unaligned_flag || !args.long_flag || args.last_mask != 0xffu) {
+      !args.unaligned_flag || !args.long_flag || args.order || args.last_mask != 0xffu) {
     return cudaErrorNotSupported;
   }
   const int ow = static_cast<int>(args.digest_bytes / 4);

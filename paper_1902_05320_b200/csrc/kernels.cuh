@@ -68,10 +68,9 @@ cudaError_t launch_hash_oneblock(const HashArgs& args, const LaunchPlan& plan,
                                  cudaStream_t stream);
 bool oneblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
 
-// Variable-length batches made of single-block messages only (kernel_short.cu): one launch
-// that does the work when the flag words say "no message reaches the rate" and returns at
-// once otherwise (the generic kernel, launched next with skip_if_short,
-// makes the opposite choice).  cudaErrorNotSupported when no instantiation matches.
+// Variable-length batches made of single-block messages only (kernel_short.cu), input order; for
+// callers that KNOW the batch is all-short (the host entries).  Returns at once if the "long" flag
+// word says otherwise.  cudaErrorNotSupported when no instantiation matches.
 cudaError_t launch_hash_short(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
 bool short_supported(int rate_lanes, uint64_t digest_bytes);
 // Equal-length form: any length below the rate (args.fixed_len), any alignment (args.aligned8).
