@@ -216,7 +216,8 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     uint32_t* flag = scratch;
     uint32_t* bucket_scratch = scratch + 8;
     uint32_t* order = bucketing ? scratch + 8 + kBucketScratchWords : nullptr;
-    CU(cudaMemsetAsync(flag, 0, 8 * sizeof(uint32_t), stream));
+    // flag words, and right behind them the histogram / cursor words of the bucketing pass
+    CU(cudaMemsetAsync(flag, 0, (8 + (bucketing ? kBucketScratchWords : 0)) * sizeof(uint32_t), stream));
     // Batches of single-block messages only have their own kernel body (kernel_short.cu).  Without
     // host knowledge, whether this is one is known on the device only (flag words): the merged
     // kernel of kernel_ragged.cu carries both bodies and branches on the flag.
@@ -228,7 +229,7 @@ int run_batch_device(int algorithm, const uint8_t* d_data, const uint64_t* d_off
     } else if (bucketing) {
       CU(launch_bucket_order(d_offsets + first, d_lengths + first, n, 8u * v.rate_lanes, order,
                              bucket_scratch, flag, stream, try_short));
-      if (launches) *launches += 3;
+      if (launches) *launches += 2;
     } else {
       CU(launch_alignment_check(d_offsets + first, d_lengths + first, n, 8u * v.rate_lanes, flag, stream));
       if (launches) *launches += 1;
@@ -471,7 +472,7 @@ int b200sha3_bucket_order_device(int algorithm, const uint64_t* d_lengths, uint6
   AsyncScratch scratch_memory;
   CU(scratch_memory.alloc((8 + kBucketScratchWords) * sizeof(uint32_t), c.stream));
   uint32_t* scratch = scratch_memory.as<uint32_t>();
-  CU(cudaMemsetAsync(scratch, 0, 8 * sizeof(uint32_t), c.stream));
+  CU(cudaMemsetAsync(scratch, 0, (8 + kBucketScratchWords) * sizeof(uint32_t), c.stream));
   // lengths double as "offsets" here: only their low bits feed the alignment flag
   CU(launch_bucket_order(d_lengths, d_lengths, static_cast<uint32_t>(count),
                          8u * kVariants[algorithm].rate_lanes, d_order, scratch + 8, scratch,

@@ -92,8 +92,7 @@ constexpr int kBucketThreads = kBucketBins;
 constexpr int kBucketItems = 4;  // messages per thread
 static_assert(kBucketThreads == kBucketBins, "one thread per bin in the block-level steps");
 
-// scratch layout: [0,256) histogram / bin base, [256,512) running cursor,
-// [512] unused.
+// scratch layout: [0, kBucketBins) histogram, [kBucketBins, 2 kBucketBins) running cursor.
 template <uint32_t RATE>
 __global__ void __launch_bounds__(kBucketThreads)
 bucket_histogram_kernel(const uint64_t* __restrict__ offsets,
@@ -127,26 +126,33 @@ bucket_histogram_kernel(const uint64_t* __restrict__ offsets,
   if (local[threadIdx.x]) atomicAdd(&hist[threadIdx.x], local[threadIdx.x]);
 }
 
-// Exclusive scan of kBucketBins values held one per thread (whole block, kBucketBins threads).
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t mine, uint32_t* tmp) {
-  const int t = threadIdx.x;
-  tmp[t] = mine;
-  __syncthreads();
-  for (int d = 1; d < kBucketBins; d <<= 1) {
-    const uint32_t add = t >= d ? tmp[t - d] : 0u;
-    __syncthreads();
-    tmp[t] += add;
-    __syncthreads();
+// Exclusive scan of kBucketBins values held one per thread (whole block of kBucketBins threads):
+// shuffle scans inside the warps, one more over the warp totals; two barriers.  `warp_sums` holds
+// kBucketBins / 32 words.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t mine, uint32_t* warp_sums) {
+  constexpr int kWarps = kBucketBins / 32;
+  static_assert(kWarps <= 32, "the warp totals are scanned by one warp");
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t v = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t up = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= static_cast<uint32_t>(d)) v += up;
   }
-  return tmp[t] - mine;
-}
-
-// Exclusive scan of the 256 bins (one block): hist -> bin base; cursor <- 0.
-__global__ void __launch_bounds__(kBucketBins)
-bucket_scan_kernel(uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor) {
-  __shared__ uint32_t tmp[kBucketBins];
-  hist[threadIdx.x] = block_exclusive_scan(hist[threadIdx.x], tmp);
-  cursor[threadIdx.x] = 0u;
+  if (lane == 31u) warp_sums[warp] = v;
+  __syncthreads();
+  if (warp == 0u) {
+    const uint32_t own = lane < kWarps ? warp_sums[lane] : 0u;
+    uint32_t s = own;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t up = __shfl_up_sync(0xffffffffu, s, d);
+      if (lane >= static_cast<uint32_t>(d)) s += up;
+    }
+    if (lane < kWarps) warp_sums[lane] = s - own;
+  }
+  __syncthreads();
+  return v - mine + warp_sums[warp];
 }
 
 // A block ranks its 2048 messages inside their bins (shared-memory counters), reserves a run
@@ -157,7 +163,7 @@ bucket_scan_kernel(uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor) {
 template <uint32_t RATE>
 __global__ void __launch_bounds__(kBucketThreads)
 bucket_scatter_kernel(const uint64_t* __restrict__ lengths, uint32_t count,
-                      const uint32_t* __restrict__ bin_base, uint32_t* __restrict__ cursor,
+                      const uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor,
                       uint32_t* __restrict__ order, const uint32_t* __restrict__ flags) {
   // `flags` is given when hash_short_kernel is launched next: an all-short batch whose
   // messages start on 8-byte boundaries is hashed there in input order (predicated 8-byte lane
@@ -166,7 +172,7 @@ bucket_scatter_kernel(const uint64_t* __restrict__ lengths, uint32_t count,
   if (flags != nullptr && flags[2] == 0u && flags[0] == 0u) return;
   constexpr int kTile = kBucketThreads * kBucketItems;
   __shared__ uint32_t local[kBucketBins];     // per-block count of the bin
-  __shared__ uint32_t tmp[kBucketBins];
+  __shared__ uint32_t warp_sums[2][kBucketBins / 32];
   __shared__ uint32_t tile_index[kTile];      // message index, bin by bin
   __shared__ uint32_t tile_target[kTile];     // where it goes in `order`
   local[threadIdx.x] = 0u;
@@ -183,8 +189,11 @@ bucket_scatter_kernel(const uint64_t* __restrict__ lengths, uint32_t count,
   }
   __syncthreads();
   const uint32_t n = local[threadIdx.x];
-  const uint32_t in_tile = block_exclusive_scan(n, tmp);  // (ends with a barrier)
-  const uint32_t in_order = n ? bin_base[threadIdx.x] + atomicAdd(&cursor[threadIdx.x], n) : 0u;
+  // where the bin starts in `order` (every block scans the 512 totals of the histogram pass
+  // itself: cheaper than one more launch) and where this block's part of it starts in the tile
+  const uint32_t bin_base = block_exclusive_scan(hist[threadIdx.x], warp_sums[0]);
+  const uint32_t in_tile = block_exclusive_scan(n, warp_sums[1]);
+  const uint32_t in_order = n ? bin_base + atomicAdd(&cursor[threadIdx.x], n) : 0u;
   __shared__ uint32_t tile_start[kBucketBins], order_start[kBucketBins];
   tile_start[threadIdx.x] = in_tile;
   order_start[threadIdx.x] = in_order;
@@ -307,15 +316,12 @@ template <uint32_t RATE>
 cudaError_t bucket_order_for_rate(const uint64_t* offsets, const uint64_t* lengths, uint32_t count,
                                   uint32_t* order, uint32_t* scratch, uint32_t* unaligned_flag,
                                   cudaStream_t stream, bool short_kernel_next) {
-  uint32_t* hist = scratch;
+  uint32_t* hist = scratch;             // zeroed by the caller, like the flag words
   uint32_t* cursor = scratch + kBucketBins;
-  cudaError_t err = cudaMemsetAsync(scratch, 0, sizeof(uint32_t) * kBucketScratchWords, stream);
-  if (err != cudaSuccess) return err;
   const unsigned per_block = kBucketThreads * kBucketItems;
   const unsigned blocks = (count + per_block - 1) / per_block;
   bucket_histogram_kernel<RATE><<<std::min(blocks, 148u * 8u), kBucketThreads, 0, stream>>>(offsets, lengths, count,
                                                                                           hist, unaligned_flag);
-  bucket_scan_kernel<<<1, kBucketBins, 0, stream>>>(hist, cursor);
   bucket_scatter_kernel<RATE><<<blocks, kBucketThreads, 0, stream>>>(
       lengths, count, hist, cursor, order, short_kernel_next ? unaligned_flag : nullptr);
   return cudaGetLastError();

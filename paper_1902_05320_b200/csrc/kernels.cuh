@@ -113,7 +113,8 @@ cudaError_t launch_permute(uint64_t* states, uint64_t count, cudaStream_t stream
 // message is at least one rate block long.  With `short_kernel_next` (hash_short_kernel is
 // launched after this pass) the order is left unwritten for a batch of single-block messages
 // with 8-byte aligned starts: that kernel takes those in input order.
-// `scratch` needs kBucketScratchWords 32-bit words.
+// `scratch` needs kBucketScratchWords 32-bit words; the caller zeroes them and the three flag
+// words (one memset when they are adjacent).
 constexpr int kBucketBins = 512;
 constexpr int kBucketScratchWords = 2 * kBucketBins + 8;
 cudaError_t launch_bucket_order(const uint64_t* offsets, const uint64_t* lengths,

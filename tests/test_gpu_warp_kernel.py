@@ -93,7 +93,7 @@ def test_auto_picks_it_for_small_multiblock_batches(oracle):
     got = device_digests(auto, 1, msgs)
     assert [r.tobytes() for r in got] == expect and auto.last_kernel_launches == 1
     got = device_digests(plain, 1, msgs)
-    assert [r.tobytes() for r in got] == expect and plain.last_kernel_launches >= 4
+    assert [r.tobytes() for r in got] == expect and plain.last_kernel_launches == 3   # histogram, scatter, hash
     # host entry (the drop-in's path) as well
     assert auto.hash_messages(1, msgs) == expect and plain.hash_messages(1, msgs) == expect
     # equal-length: multi-block -> warp kernel, same digests as the generic kernel
