@@ -315,6 +315,84 @@ int finish_call(int rc, SlotPipeline& pipe, HostIo& io, const Config& c, uint32_
   return B200SHA3_OK;
 }
 
+// Few LONG equal-length messages from pinned host memory: the batch is latency bound (a sponge is
+// sequential per message; the warp-per-state kernels need ~2 us per block whatever the count),
+// so cutting it into chunks of MESSAGES only lines the chunks' latencies up behind one another.
+// Cut every message into PIECES instead: piece k of all messages is one strided copy
+// (cudaMemcpy2DAsync: pitch = message length), absorbed into device-resident sponge states by
+// the incremental warp kernel (kernel_stream_warp.cu) while piece k + 1 is on the link.  The call
+// then costs max(copy, hashing) + one piece instead of copy + hashing (1024 x 1 MiB: 36 -> 22 ms).
+// Pieces are whole rate blocks, so every update leaves the byte position at 0.
+int hash_fixed_in_pieces(int algorithm, const uint8_t* data, uint64_t msg_len, uint64_t count,
+                         uint64_t xof_output_bits, uint64_t digest_bytes, uint8_t* digests, const Config& c) {
+  const Variant& v = kVariants[algorithm];
+  const uint64_t rate = 8u * static_cast<uint64_t>(v.rate_lanes);
+  // ~16 pieces per message, at least 64 KiB each (a piece is one launch: >= ~1 ms of hashing)
+  uint64_t piece = std::max<uint64_t>(64u << 10, msg_len / 16);
+  piece = std::max<uint64_t>(rate, piece / rate * rate);
+  const uint64_t pieces = (msg_len + piece - 1) / piece;
+  SlotPipeline pipe(kPipelineSlots, c.device_ms != nullptr);
+  CU(pipe.init());
+  HostIo io;
+  CU(io.init(nullptr, 0, digests, count * digest_bytes));
+  uint8_t* d_piece[kPipelineSlots] = {};
+  for (int s = 0; s < pipe.slots(); ++s) CU(pipe.alloc(s, &d_piece[s], count * piece));
+  uint2* lanes = nullptr;
+  uint32_t* pos = nullptr;
+  uint8_t* d_out = nullptr;
+  CU(pipe.alloc(0, &lanes, 25 * count * sizeof(uint2)));
+  CU(pipe.alloc(0, &pos, count * sizeof(uint32_t)));
+  CU(pipe.alloc(0, &d_out, count * digest_bytes));
+  CU(cudaMemsetAsync(lanes, 0, 25 * count * sizeof(uint2), pipe.stream(0)));
+  CU(cudaMemsetAsync(pos, 0, count * sizeof(uint32_t), pipe.stream(0)));
+  // updates run in piece order: each waits for the event of the one before it
+  cudaEvent_t hashed[kPipelineSlots] = {};
+  struct EventGuard {
+    cudaEvent_t* e;
+    ~EventGuard() {
+      for (int s = 0; s < kPipelineSlots; ++s) {
+        if (e[s]) cudaEventDestroy(e[s]);
+      }
+    }
+  } guard{hashed};
+  for (int s = 0; s < pipe.slots(); ++s) CU(cudaEventCreateWithFlags(&hashed[s], cudaEventDisableTiming));
+  CU(cudaEventRecord(hashed[pipe.slots() - 1], pipe.stream(0)));  // "piece -1": the states are zeroed
+  int rc = B200SHA3_OK;
+  uint32_t launches = 0;
+  int last = 0;
+  for (uint64_t k = 0; k < pieces && rc == B200SHA3_OK; ++k) {
+    const int s = static_cast<int>(k % pipe.slots());
+    const int before = static_cast<int>((k + pipe.slots() - 1) % pipe.slots());
+    const uint64_t width = std::min(piece, msg_len - k * piece);
+    cudaStream_t stream = pipe.stream(s);
+    cudaError_t e = cudaMemcpy2DAsync(d_piece[s], width, data + k * piece, msg_len, width, count,
+                                      cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, hashed[before], 0);
+    if (e == cudaSuccess) e = pipe.begin_kernels(s);
+    if (e == cudaSuccess) {
+      e = launch_states_update_warp(v.rate_lanes, lanes, pos, count, d_piece[s], nullptr, nullptr, width, stream);
+    }
+    if (e == cudaSuccess) e = pipe.end_kernels(s);
+    if (e == cudaSuccess) e = cudaEventRecord(hashed[s], stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "piece pipeline");
+    launches += 1;
+    last = s;
+  }
+  if (rc == B200SHA3_OK) {
+    cudaStream_t stream = pipe.stream(last);
+    cudaError_t e = pipe.begin_kernels(last);
+    if (e == cudaSuccess) {
+      e = launch_states_finish_warp(v.rate_lanes, lanes, pos, count, v.head, d_out, digest_bytes,
+                                    last_byte_mask(algorithm, xof_output_bits), stream);
+    }
+    if (e == cudaSuccess) e = pipe.end_kernels(last);
+    if (e == cudaSuccess) e = io.d2h(digests, d_out, count * digest_bytes, stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "piece pipeline");
+    launches += 1;
+  }
+  return finish_call(rc, pipe, io, c, launches);
+}
+
 }  // namespace
 
 extern "C" {
@@ -336,6 +414,13 @@ int b200sha3_hash_fixed(int algorithm, const uint8_t* data, uint64_t msg_len, ui
   if (c.stream) CU(cudaStreamSynchronize(c.stream));
 
   const bool pipelined = (c.flags & B200SHA3_FLAG_NO_PIPELINE) == 0;
+  // few long messages (warp-per-state territory) from pinned memory: pipeline over PIECES of
+  // the messages instead of over message ranges
+  if (pipelined && few_enough_for_warps(count, c) && c.kernel == B200SHA3_KERNEL_AUTO && count >= 2 &&
+      msg_len >= (256u << 10) && msg_len < (1ull << 31) && count * msg_len >= (64ull << 20) &&
+      !is_pageable(data)) {
+    return hash_fixed_in_pieces(algorithm, data, msg_len, count, xof_output_bits, digest_bytes, digests, c);
+  }
   const uint64_t unit = std::max<uint64_t>(1, msg_len + digest_bytes);
   uint64_t chunk = pipelined ? chunk_target_bytes(unit) / unit : count;
   chunk = std::min(std::max<uint64_t>(chunk, 16), count);

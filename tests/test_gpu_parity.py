@@ -771,3 +771,36 @@ def test_device_entries_can_be_captured_in_a_cuda_graph(oracle):
         torch.cuda.synchronize()
         assert (out_var.cpu().numpy() == oracle.hash_batch(1, blob2, offsets, lengths, workers=4)).all()
         assert (out_fix.cpu().numpy() == oracle.hash_batch(1, fixed2, fixed_len=64, count=4096, workers=4)).all()
+
+
+@pytest.mark.parametrize("algorithm,bits", [(1, 0), (3, 0), (4, 1027)])
+def test_few_long_messages_from_pinned_memory_are_hashed_in_pieces(big_engine, algorithm, bits):
+    """Few long equal-length messages in pinned host memory take the piece pipeline of the
+    fixed-length host entry (strided copies of one piece of every message, absorbed by the
+    incremental warp kernel while the next piece is on the link): same digests as hashlib, as
+    the unpipelined call and as the device entry; lengths that are no multiple of the rate or
+    of the piece size."""
+    import hashlib
+    import torch
+    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200.engine import FLAG_NO_PIPELINE
+    engine = big_engine
+    names = ["sha3_224", "sha3_256", "sha3_384", "sha3_512", "shake_128", "shake_256"]
+    for count, msg_len in ((96, 1_000_003), (700, 300_001)):
+        host = torch.randint(0, 256, (count * msg_len,), dtype=torch.uint8).pin_memory()
+        nbytes = (bits + 7) // 8 if algorithm >= 4 else (28, 32, 48, 64)[algorithm]
+        out = torch.zeros(count * nbytes, dtype=torch.uint8).pin_memory()
+        engine.hash_fixed_ptr(algorithm, host.data_ptr(), msg_len, count, out.data_ptr(), bits)
+        assert engine.last_kernel_launches > 3                  # one update per piece + the finish
+        got = out.view(count, nbytes).numpy()
+        plain = Engine(flags=FLAG_NO_PIPELINE).hash_fixed(algorithm, host.numpy(), msg_len, count, bits)
+        assert (got == plain).all()
+        dev = engine.hash_fixed(algorithm, host.cuda(), msg_len, count, bits).cpu().numpy()
+        assert (got == dev).all()
+        raw = host.numpy()
+        for i in (0, 1, count // 2, count - 1):
+            h = hashlib.new(names[algorithm], raw[i * msg_len:(i + 1) * msg_len].tobytes())
+            want = h.digest(nbytes) if algorithm >= 4 else h.digest()
+            if algorithm >= 4 and bits % 8:
+                want = want[:-1] + bytes([want[-1] & ((1 << (bits % 8)) - 1)])
+            assert got[i].tobytes() == want
