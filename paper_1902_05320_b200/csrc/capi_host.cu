@@ -331,7 +331,7 @@ int hash_fixed_in_pieces(int algorithm, const uint8_t* data, uint64_t msg_len, u
   uint64_t piece = std::max<uint64_t>(64u << 10, msg_len / 16);
   piece = std::max<uint64_t>(rate, piece / rate * rate);
   const uint64_t pieces = (msg_len + piece - 1) / piece;
-  SlotPipeline pipe(kPipelineSlots, c.device_ms != nullptr);
+  SlotPipeline pipe(kPipelineSlots, /*timed=*/false);  // (kernel time: own events, below)
   CU(pipe.init());
   HostIo io;
   CU(io.init(nullptr, 0, digests, count * digest_bytes));
@@ -345,17 +345,24 @@ int hash_fixed_in_pieces(int algorithm, const uint8_t* data, uint64_t msg_len, u
   CU(pipe.alloc(0, &d_out, count * digest_bytes));
   CU(cudaMemsetAsync(lanes, 0, 25 * count * sizeof(uint2), pipe.stream(0)));
   CU(cudaMemsetAsync(pos, 0, count * sizeof(uint32_t), pipe.stream(0)));
-  // updates run in piece order: each waits for the event of the one before it
-  cudaEvent_t hashed[kPipelineSlots] = {};
+  // updates run in piece order: each waits for the event of the one before it.  Kernel time
+  // (cfg->device_ms) is bracketed per piece with its own event pair, collected after the drain:
+  // the slots' shared pairs would make the host wait for piece k - 3 before it may enqueue piece k.
+  const bool timed = c.device_ms != nullptr;
+  std::vector<cudaEvent_t> events(pipe.slots() + (timed ? 2 * (pieces + 1) : 0), nullptr);
   struct EventGuard {
-    cudaEvent_t* e;
+    std::vector<cudaEvent_t>& e;
     ~EventGuard() {
-      for (int s = 0; s < kPipelineSlots; ++s) {
-        if (e[s]) cudaEventDestroy(e[s]);
+      for (cudaEvent_t ev : e) {
+        if (ev) cudaEventDestroy(ev);
       }
     }
-  } guard{hashed};
-  for (int s = 0; s < pipe.slots(); ++s) CU(cudaEventCreateWithFlags(&hashed[s], cudaEventDisableTiming));
+  } guard{events};
+  for (size_t i = 0; i < events.size(); ++i) {
+    CU(cudaEventCreateWithFlags(&events[i], i < static_cast<size_t>(pipe.slots()) ? cudaEventDisableTiming : cudaEventDefault));
+  }
+  cudaEvent_t* hashed = events.data();
+  cudaEvent_t* bracket = events.data() + pipe.slots();
   CU(cudaEventRecord(hashed[pipe.slots() - 1], pipe.stream(0)));  // "piece -1": the states are zeroed
   int rc = B200SHA3_OK;
   uint32_t launches = 0;
@@ -368,11 +375,11 @@ int hash_fixed_in_pieces(int algorithm, const uint8_t* data, uint64_t msg_len, u
     cudaError_t e = cudaMemcpy2DAsync(d_piece[s], width, data + k * piece, msg_len, width, count,
                                       cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, hashed[before], 0);
-    if (e == cudaSuccess) e = pipe.begin_kernels(s);
+    if (e == cudaSuccess && timed) e = cudaEventRecord(bracket[2 * k], stream);
     if (e == cudaSuccess) {
       e = launch_states_update_warp(v.rate_lanes, lanes, pos, count, d_piece[s], nullptr, nullptr, width, stream);
     }
-    if (e == cudaSuccess) e = pipe.end_kernels(s);
+    if (e == cudaSuccess && timed) e = cudaEventRecord(bracket[2 * k + 1], stream);
     if (e == cudaSuccess) e = cudaEventRecord(hashed[s], stream);
     if (e != cudaSuccess) rc = cuda_fail(e, "piece pipeline");
     launches += 1;
@@ -380,17 +387,27 @@ int hash_fixed_in_pieces(int algorithm, const uint8_t* data, uint64_t msg_len, u
   }
   if (rc == B200SHA3_OK) {
     cudaStream_t stream = pipe.stream(last);
-    cudaError_t e = pipe.begin_kernels(last);
+    cudaError_t e = timed ? cudaEventRecord(bracket[2 * pieces], stream) : cudaSuccess;
     if (e == cudaSuccess) {
       e = launch_states_finish_warp(v.rate_lanes, lanes, pos, count, v.head, d_out, digest_bytes,
                                     last_byte_mask(algorithm, xof_output_bits), stream);
     }
-    if (e == cudaSuccess) e = pipe.end_kernels(last);
+    if (e == cudaSuccess && timed) e = cudaEventRecord(bracket[2 * pieces + 1], stream);
     if (e == cudaSuccess) e = io.d2h(digests, d_out, count * digest_bytes, stream);
     if (e != cudaSuccess) rc = cuda_fail(e, "piece pipeline");
     launches += 1;
   }
-  return finish_call(rc, pipe, io, c, launches);
+  rc = finish_call(rc, pipe, io, c, launches);  // drains the streams
+  if (rc == B200SHA3_OK && timed) {
+    double kernel_ms = 0.0;
+    for (uint64_t k = 0; k <= pieces; ++k) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, bracket[2 * k], bracket[2 * k + 1]));
+      kernel_ms += ms;
+    }
+    *c.device_ms = kernel_ms;
+  }
+  return rc;
 }
 
 }  // namespace
