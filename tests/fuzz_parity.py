@@ -17,7 +17,7 @@ import torch  # noqa: E402
 from oracle.binding import Oracle  # noqa: E402
 from paper_1902_05320_b200 import BatchHasher, Engine  # noqa: E402
 from paper_1902_05320_b200.engine import (FLAG_NO_BUCKETING, FLAG_NO_PIPELINE, FLAG_NO_WARP_KERNEL,  # noqa: E402
-                                          KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STAGED, KERNEL_WARP)
+                                          KERNEL_AUTO, KERNEL_GENERIC, KERNEL_PAIR, KERNEL_STAGED, KERNEL_WARP)
 
 
 def random_lengths(rng, count, rate):
@@ -56,7 +56,7 @@ def main():
             pos += int(lengths[i])
         data = rng.integers(0, 256, pos + 16, dtype=np.uint8)
         expect = oracle.hash_batch(alg, data, offsets, lengths, xof_bits=bits, workers=8)
-        entry = str(rng.choice(["device", "device_nobucket", "device_staged", "device_warp", "host", "host_nopipe",
+        entry = str(rng.choice(["device", "device_nobucket", "device_staged", "device_warp", "device_pair", "host", "host_nopipe",
                                 "fixed_device", "fixed_host", "incremental"]))
         # small batches take the warp-per-state kernel by default: half of the cases switch it off
         # so that the one-message-per-thread kernels see small batches too
@@ -65,7 +65,7 @@ def main():
             n = int(lengths[0])
             fixed = rng.integers(0, 256, max(count * n, 1) + 16, dtype=np.uint8)
             expect = oracle.hash_batch(alg, fixed, fixed_len=n, count=count, xof_bits=bits, workers=8)
-            kernel = int(rng.choice([KERNEL_AUTO, KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STAGED, KERNEL_WARP]))
+            kernel = int(rng.choice([KERNEL_AUTO, KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STAGED, KERNEL_WARP, KERNEL_PAIR]))
             eng = Engine(kernel=kernel, flags=no_warp)
             if entry == "fixed_device":
                 got = eng.hash_fixed(alg, torch.from_numpy(fixed).cuda(), n, count, bits).cpu().numpy()
@@ -82,7 +82,7 @@ def main():
             h.close()
         elif entry.startswith("device"):
             flags = (FLAG_NO_BUCKETING if entry == "device_nobucket" else 0) | no_warp
-            kernel = {"device_staged": KERNEL_STAGED, "device_warp": KERNEL_WARP}.get(entry, KERNEL_AUTO)
+            kernel = {"device_staged": KERNEL_STAGED, "device_warp": KERNEL_WARP, "device_pair": KERNEL_PAIR}.get(entry, KERNEL_AUTO)
             eng = Engine(flags=flags, kernel=kernel)
             got = eng.hash_batch(alg, torch.from_numpy(data).cuda(), torch.from_numpy(offsets.astype(np.int64)).cuda(),
                                  torch.from_numpy(lengths.astype(np.int64)).cuda(), bits).cpu().numpy()
