@@ -327,8 +327,10 @@ int hash_fixed_in_pieces(int algorithm, const uint8_t* data, uint64_t msg_len, u
                          uint64_t xof_output_bits, uint64_t digest_bytes, uint8_t* digests, const Config& c) {
   const Variant& v = kVariants[algorithm];
   const uint64_t rate = 8u * static_cast<uint64_t>(v.rate_lanes);
-  // ~16 pieces per message, at least 64 KiB each (a piece is one launch: >= ~1 ms of hashing)
+  // ~16 pieces per message, at least 64 KiB each (a piece is one launch: >= ~1 ms of hashing), at
+  // most 256 MiB per piece of the whole batch (three device buffers of that size)
   uint64_t piece = std::max<uint64_t>(64u << 10, msg_len / 16);
+  if (count * piece > (256ull << 20)) piece = std::max<uint64_t>(64u << 10, (256ull << 20) / count);
   piece = std::max<uint64_t>(rate, piece / rate * rate);
   const uint64_t pieces = (msg_len + piece - 1) / piece;
   SlotPipeline pipe(kPipelineSlots, /*timed=*/false);  // (kernel time: own events, below)
