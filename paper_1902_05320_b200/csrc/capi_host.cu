@@ -350,8 +350,11 @@ int hash_fixed_in_pieces(int algorithm, const uint8_t* data, uint64_t msg_len, u
   // updates run in piece order: each waits for the event of the one before it.  Kernel time
   // (cfg->device_ms) is bracketed per piece with its own event pair, collected after the drain:
   // the slots' shared pairs would make the host wait for piece k - 3 before it may enqueue piece k.
+  // (Beyond 512 pieces one pair brackets the whole run of updates instead: copy waits included.)
   const bool timed = c.device_ms != nullptr;
-  std::vector<cudaEvent_t> events(pipe.slots() + (timed ? 2 * (pieces + 1) : 0), nullptr);
+  const bool per_piece = timed && pieces <= 512;
+  const uint64_t brackets = !timed ? 0 : per_piece ? pieces + 1 : 1;
+  std::vector<cudaEvent_t> events(pipe.slots() + 2 * brackets, nullptr);
   struct EventGuard {
     std::vector<cudaEvent_t>& e;
     ~EventGuard() {
@@ -377,11 +380,11 @@ int hash_fixed_in_pieces(int algorithm, const uint8_t* data, uint64_t msg_len, u
     cudaError_t e = cudaMemcpy2DAsync(d_piece[s], width, data + k * piece, msg_len, width, count,
                                       cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, hashed[before], 0);
-    if (e == cudaSuccess && timed) e = cudaEventRecord(bracket[2 * k], stream);
+    if (e == cudaSuccess && (per_piece || (timed && k == 0))) e = cudaEventRecord(bracket[per_piece ? 2 * k : 0], stream);
     if (e == cudaSuccess) {
       e = launch_states_update_warp(v.rate_lanes, lanes, pos, count, d_piece[s], nullptr, nullptr, width, stream);
     }
-    if (e == cudaSuccess && timed) e = cudaEventRecord(bracket[2 * k + 1], stream);
+    if (e == cudaSuccess && per_piece) e = cudaEventRecord(bracket[2 * k + 1], stream);
     if (e == cudaSuccess) e = cudaEventRecord(hashed[s], stream);
     if (e != cudaSuccess) rc = cuda_fail(e, "piece pipeline");
     launches += 1;
@@ -389,12 +392,12 @@ int hash_fixed_in_pieces(int algorithm, const uint8_t* data, uint64_t msg_len, u
   }
   if (rc == B200SHA3_OK) {
     cudaStream_t stream = pipe.stream(last);
-    cudaError_t e = timed ? cudaEventRecord(bracket[2 * pieces], stream) : cudaSuccess;
+    cudaError_t e = per_piece ? cudaEventRecord(bracket[2 * pieces], stream) : cudaSuccess;
     if (e == cudaSuccess) {
       e = launch_states_finish_warp(v.rate_lanes, lanes, pos, count, v.head, d_out, digest_bytes,
                                     last_byte_mask(algorithm, xof_output_bits), stream);
     }
-    if (e == cudaSuccess && timed) e = cudaEventRecord(bracket[2 * pieces + 1], stream);
+    if (e == cudaSuccess && timed) e = cudaEventRecord(bracket[per_piece ? 2 * pieces + 1 : 1], stream);
     if (e == cudaSuccess) e = io.d2h(digests, d_out, count * digest_bytes, stream);
     if (e != cudaSuccess) rc = cuda_fail(e, "piece pipeline");
     launches += 1;
@@ -402,7 +405,7 @@ int hash_fixed_in_pieces(int algorithm, const uint8_t* data, uint64_t msg_len, u
   rc = finish_call(rc, pipe, io, c, launches);  // drains the streams
   if (rc == B200SHA3_OK && timed) {
     double kernel_ms = 0.0;
-    for (uint64_t k = 0; k <= pieces; ++k) {
+    for (uint64_t k = 0; k < brackets; ++k) {
       float ms = 0.f;
       CU(cudaEventElapsedTime(&ms, bracket[2 * k], bracket[2 * k + 1]));
       kernel_ms += ms;
