@@ -58,9 +58,14 @@ class StreamCache {
 
 thread_local StreamCache t_streams;
 
-// One message is one thread, so a chunk must also carry enough MESSAGES to fill the GPU: for
-// long messages the byte target grows until a chunk holds ~2^16 of them (2048 warps), up to
-// 1 GiB (three slots of that are still < 2 % of the HBM).
+// A chunk must also carry enough MESSAGES: for long messages the byte target grows until a chunk
+// holds ~2^11 of them, up to 1 GiB (three slots of that are still < 2 % of the HBM).  2^11, not
+// more: a chunk of a few thousand multi-block messages runs on the warp-per-state kernel at
+// ~2-4 us per block, which is about what its copy takes up to ~64 KiB per message (so copy and
+// hashing of consecutive chunks overlap); round 1 grew chunks to 2^16 messages for the
+// one-message-per-thread kernel and 2^14 x 64 KiB went through as ONE chunk, copy then hash.
+// Beyond ~64 KiB per message a chunk is latency bound whatever it holds, and the 1 GiB cap
+// (or hash_fixed_in_pieces below, for a whole batch of few long messages) applies.
 uint64_t chunk_target_bytes(uint64_t avg_message_bytes) {
   static const long env_mib = [] {
     const char* env = std::getenv("B200SHA3_CHUNK_MIB");
@@ -68,7 +73,7 @@ uint64_t chunk_target_bytes(uint64_t avg_message_bytes) {
   }();
   if (env_mib > 0) return static_cast<uint64_t>(env_mib) << 20;
   const uint64_t base = 64ull << 20, cap = 1ull << 30;
-  const uint64_t want = avg_message_bytes > (cap >> 16) ? cap : avg_message_bytes << 16;
+  const uint64_t want = avg_message_bytes > (cap >> 11) ? cap : avg_message_bytes << 11;
   return std::min(std::max(want, base), cap);
 }
 

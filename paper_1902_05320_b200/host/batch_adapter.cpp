@@ -290,7 +290,7 @@ class BatchPipeline {
   static constexpr std::uint64_t kChunkBytes = (32ull << 20) >> kScale;   // input + output per device call ...
   static constexpr std::uint64_t kMinChunkBytes = (2ull << 20) >> kScale; // ... at least this ...
   static constexpr std::uint64_t kMinChunks = 8;                          // ... aiming at this many chunks
-  static constexpr std::uint64_t kChunkMinMessages = (1u << 15) >> kScale;  // ... grown to hold this many messages
+  static constexpr std::uint64_t kChunkMinMessages = (1u << 11) >> kScale;  // ... grown to hold this many messages
   static constexpr std::uint64_t kMaxChunkBytes = (1ull << 30) >> kScale;   // ... up to this
   static constexpr std::uint64_t kPoolMinBytes = (4ull << 20) >> kScale;  // below: the caller works alone
   static constexpr std::size_t kParallelScanMin = (1u << 18) >> kScale;   // messages
@@ -364,7 +364,8 @@ class BatchPipeline {
     }
     const std::size_t ndev = std::max<std::size_t>(1, device_.devices.size());
     // A chunk is one kernel launch with one thread per message: long messages get larger
-    // chunks so that a launch still carries ~2^15 of them.
+    // chunks so that a launch still carries ~2^11 of them (warp-per-state kernel territory: a
+    // chunk's hashing then takes about as long as its copy up to ~64 KiB per message).
     static const std::uint64_t min_chunks = [] {  // B200SHA3_ADAPTER_MIN_CHUNKS: experiment knob
       const char* env = std::getenv("B200SHA3_ADAPTER_MIN_CHUNKS");
       const long n = env ? std::atol(env) : 0;
