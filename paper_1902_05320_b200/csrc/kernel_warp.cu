@@ -14,14 +14,15 @@
 //   pi+chi  thread (x, y) fetches the three rho outputs that pi moves to (x, y), (x+1, y)
 //           and (x+2, y) -- three shuffles with per-thread constant sources -- and applies
 //           chi; iota on lane 0 through a mask.
-//   = 9 64-bit shuffles (18 SHFL) in three dependent stages + ~16 ALU instructions per round,
-//   so one permutation is ~24 x 3 shuffle latencies instead of ~4200 ALU issue slots.
+//   = 9 64-bit shuffles (18 SHFL) in three dependent stages + ~16 ALU instructions per round:
+//   measured 3994 cycles per permutation (24 x (18 x ~4 cycles of SHFL issue + 3 x ~28 of
+//   latency + the dependent ALU instructions)) against ~10 000 in one thread.
 //
 // Absorb is one coalesced 8 x RL-byte read per block (thread t loads lane t; the next block
 // is prefetched before the rounds of the current one), squeeze one coalesced write.
 // Throughput per message is far below the one-thread kernels (25 of 32 lanes, shuffle
-// bound), so capi.cu picks this kernel only when the batch could not fill the machine
-// anyway (see kWarpKernelMaxCount there).
+// bound: ~1 SHFL per clock per SM), so capi.cu picks this kernel only when the batch could not
+// fill the machine anyway (warp_kernel_max_count() there: 2816 messages).
 #include "kernels.cuh"
 #include "warp_state.cuh"
 
