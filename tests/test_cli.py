@@ -225,3 +225,15 @@ def test_reference_parser_on_our_backend(tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
     seen = sum(int(row.rsplit(" ", 1)[1].split("/")[0]) for row in r.stdout.strip().splitlines())
     assert seen == total == 892
+
+
+@pytest.mark.gpu
+def test_bench_packed_layout_on_few_long_messages(cli):
+    """256 x 1 MiB from pinned memory: the piece pipeline of the fixed-length host entry, with its
+    per-piece kernel timing (cfg->device_ms) -- kernel time is reported and is less than the call."""
+    r = run(cli, "bench", "--message-size", "1048576", "--sizes", "268435456", "--layout", "packed")
+    assert r.returncode == 0, r.stdout + r.stderr
+    cols = r.stdout.strip().splitlines()[-1].split()
+    assert int(cols[2]) == 256 and cols[3] == "cuda-packed"
+    time_s, kernels_s = float(cols[4]), float(cols[7])
+    assert 0.010 < kernels_s < time_s < 0.060          # ~16 ms of hashing inside a ~17-20 ms call
