@@ -509,6 +509,18 @@ def main():
         data[:e2e_count * MSG_LEN].copy_(host_in, non_blocking=True)
         torch.cuda.synchronize()
         plain_h2d_gbs = e2e_count * MSG_LEN / (time.perf_counter() - t0) / 1e9
+        # ... and the ceiling of the call's shape: the same input and output buffers copied BOTH
+        # ways at once on two streams, no hashing (tools/microbench/pcie_duplex.cu is the
+        # stand-alone form).  H2D runs slower under opposite traffic than alone.
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s_in):
+            data[:e2e_count * MSG_LEN].copy_(host_in, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            host_out.copy_(digests.view(-1)[:e2e_count * DIGEST_BYTES], non_blocking=True)
+        torch.cuda.synchronize()
+        duplex_seconds = max_over_ranks(time.perf_counter() - t0)
         e2e_total = e2e_count * world if e2e_count != count else total
         e2e = {"value": e2e_total * e2e_steps / e2e_seconds, "unit": "hashes/s",
                "h2d_bytes_per_step": e2e_total * MSG_LEN, "d2h_bytes_per_step": e2e_total * DIGEST_BYTES,
@@ -518,6 +530,13 @@ def main():
                "pcie": {"h2d_gb_per_s_inside_pipeline": e2e_count * MSG_LEN * e2e_steps / e2e_seconds / 1e9,
                         "d2h_gb_per_s_inside_pipeline": e2e_count * DIGEST_BYTES * e2e_steps / e2e_seconds / 1e9,
                         "h2d_gb_per_s_plain_pinned_copy": plain_h2d_gbs,
+                        "duplex_plain_copies": {
+                            "ms": duplex_seconds * 1e3,
+                            "h2d_gb_per_s": e2e_count * MSG_LEN / duplex_seconds / 1e9,
+                            "d2h_gb_per_s": e2e_count * DIGEST_BYTES / duplex_seconds / 1e9,
+                            "note": "input and output buffers of one step copied both ways at once, no "
+                                    "hashing: the floor for one e2e step on this link"},
+                        "e2e_step_over_duplex_copies": e2e_seconds / e2e_steps / duplex_seconds,
                         "note": "per rank; e2e is bound by the host link, not by the kernel"},
                "note": "b200sha3_hash_fixed on pinned host buffers: chunked H2D / kernel / D2H "
                        "pipeline inside the call; wall clock, max over ranks"}
