@@ -35,6 +35,9 @@ def test_bench_line_shape_at_reduced_size():
     e2e = line["e2e"]
     assert e2e["h2d_bytes_per_step"] == (1 << 22) * 64 and e2e["d2h_bytes_per_step"] == (1 << 22) * 32
     assert e2e["digests_match_device_path"] is True and 0 < e2e["value"] < line["value"]
+    # the link's ceiling for the call's shape, measured in the same run: both plain copies at once
+    duplex = e2e["pcie"]["duplex_plain_copies"]
+    assert duplex["ms"] > 0 and duplex["h2d_gb_per_s"] > 0 and e2e["pcie"]["e2e_step_over_duplex_copies"] > 0
     names = [c["config"] for c in line["configs"]]
     assert [n.split(":")[0] for n in names] == ["cfg1", "cfg2", "cfg2", "cfg2", "cfg3", "cfg3", "cfg4",
                                                 "few long messages"]

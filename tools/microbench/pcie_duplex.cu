@@ -13,6 +13,10 @@
 //   duplex_chunked  both at once, cut into chunks on two streams (the shape of the pipeline)
 //   duplex_wc       duplex_chunked with the input in write-combined memory
 //   zero_copy_read  a kernel reading the mapped input with 16-byte loads (no copy engine)
+//   zero_copy_write / duplex_h2d_copy_with_zero_copy_write
+//                   a kernel storing the output straight into mapped host memory, alone and
+//                   while the copy engine brings the input in
+// The *_gbs figures of the duplex rows are bytes over the time of the WHOLE row (both copies).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -45,6 +49,10 @@ __global__ void read_kernel(const uint4* __restrict__ src, size_t n, uint4* sink
   if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678u) *sink = acc;
 }
 
+__global__ void write_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, size_t n) {
+  for (size_t i = blockIdx.x * size_t{blockDim.x} + threadIdx.x; i < n; i += size_t{gridDim.x} * blockDim.x) dst[i] = src[i];
+}
+
 template <class F>
 static double best_of(int reps, F&& f) {
   double best = 1e30;
@@ -65,7 +73,7 @@ int main(int argc, char** argv) {
   uint8_t *h_in, *h_wc, *h_out, *d_in, *d_out;
   CU(cudaHostAlloc(reinterpret_cast<void**>(&h_in), in_bytes, cudaHostAllocDefault));
   CU(cudaHostAlloc(reinterpret_cast<void**>(&h_wc), in_bytes, cudaHostAllocWriteCombined | cudaHostAllocMapped));
-  CU(cudaHostAlloc(reinterpret_cast<void**>(&h_out), out_bytes, cudaHostAllocDefault));
+  CU(cudaHostAlloc(reinterpret_cast<void**>(&h_out), out_bytes, cudaHostAllocMapped));
   CU(cudaMalloc(reinterpret_cast<void**>(&d_in), in_bytes));
   CU(cudaMalloc(reinterpret_cast<void**>(&d_out), out_bytes));
   std::memset(h_in, 1, in_bytes);
@@ -101,15 +109,36 @@ int main(int argc, char** argv) {
     read_kernel<<<148 * 8, 256, 0, s_in>>>(reinterpret_cast<const uint4*>(mapped), in_bytes / 16, sink);
   });
   CU(cudaGetLastError());
+  // the output written by a kernel straight into mapped host memory (posted writes, no copy
+  // engine) while the copy engine brings the input in; and alone.  Few blocks: a hash kernel
+  // would produce its digests at a trickle, not in one burst.
+  uint8_t* mapped_out;
+  CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped_out), h_out, 0));
+  const double zc_write = best_of(reps, [&] {
+    write_kernel<<<148, 256, 0, s_out>>>(reinterpret_cast<uint4*>(mapped_out), reinterpret_cast<const uint4*>(d_out), out_bytes / 16);
+  });
+  const double dup_zc_write = best_of(reps, [&] {
+    CU(cudaMemcpyAsync(d_in, h_in, in_bytes, cudaMemcpyHostToDevice, s_in));
+    write_kernel<<<148, 256, 0, s_out>>>(reinterpret_cast<uint4*>(mapped_out), reinterpret_cast<const uint4*>(d_out), out_bytes / 16);
+  });
+  // H2D alone while NOTHING goes the other way but with the D2H done afterwards (serial)
+  const double serial = best_of(reps, [&] {
+    CU(cudaMemcpyAsync(d_in, h_in, in_bytes, cudaMemcpyHostToDevice, s_in));
+    CU(cudaStreamSynchronize(s_in));
+    CU(cudaMemcpyAsync(h_out, d_out, out_bytes, cudaMemcpyDeviceToHost, s_out));
+  });
+  CU(cudaGetLastError());
   auto gbs = [](size_t bytes, double s) { return bytes / s / 1e9; };
   std::printf(
       "{\"in_gib\": %zu, \"chunk_mib\": %zu, \"h2d_pinned_gbs\": %.2f, \"h2d_wc_gbs\": %.2f, \"d2h_pinned_gbs\": %.2f, "
       "\"duplex_whole\": {\"seconds\": %.4f, \"h2d_gbs\": %.2f, \"d2h_gbs\": %.2f}, "
       "\"duplex_chunked\": {\"seconds\": %.4f, \"h2d_gbs\": %.2f, \"d2h_gbs\": %.2f}, "
       "\"duplex_wc\": {\"seconds\": %.4f, \"h2d_gbs\": %.2f, \"d2h_gbs\": %.2f}, "
-      "\"zero_copy_read_gbs\": %.2f}\n",
+      "\"zero_copy_read_gbs\": %.2f, \"zero_copy_write_gbs\": %.2f, "
+      "\"duplex_h2d_copy_with_zero_copy_write\": {\"seconds\": %.4f, \"h2d_gbs\": %.2f}, \"serial_h2d_then_d2h_seconds\": %.4f}\n",
       gib_in, chunk_in >> 20, gbs(in_bytes, h2d), gbs(in_bytes, h2d_wc), gbs(out_bytes, d2h), dup_whole,
       gbs(in_bytes, dup_whole), gbs(out_bytes, dup_whole), dup_chunk, gbs(in_bytes, dup_chunk),
-      gbs(out_bytes, dup_chunk), dup_wc, gbs(in_bytes, dup_wc), gbs(out_bytes, dup_wc), gbs(in_bytes, zc));
+      gbs(out_bytes, dup_chunk), dup_wc, gbs(in_bytes, dup_wc), gbs(out_bytes, dup_wc), gbs(in_bytes, zc), gbs(out_bytes, zc_write), dup_zc_write,
+      gbs(in_bytes, dup_zc_write), serial);
   return 0;
 }
