@@ -50,6 +50,9 @@ def parse_args():
     ap.add_argument("--no-probe", action="store_true")
     ap.add_argument("--no-dropin", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the cfg1..cfg4 device-time points")
+    ap.add_argument("--gather-digests", action="store_true",
+                    help="N>1: after the timed region, all-gather the digests to every rank (the optional "
+                         "step after the hot path, SURVEY.md 8(e)) and report its time")
     ap.add_argument("--quick-configs", action="store_true", help=argparse.SUPPRESS)
     # validation only (one-GPU box): run N ranks on the SAME device with a gloo process group
     # to exercise the multi-rank code path; numbers from such a run are not benchmark values
@@ -474,6 +477,23 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
     checksum = int(t.item()) & (2**64 - 1)
 
+    # ---- optional: digests of the whole batch on every rank (NCCL all-gather over NVLink; the
+    # hot path never needs it -- digests stay with their shard unless requested) ----------
+    gather = None
+    if args.gather_digests and world > 1:
+        from paper_1902_05320_b200.sharding import gather_digests
+        local = digests.cpu() if args.share_gpu else digests
+        barrier()
+        t0 = time.perf_counter()
+        everything = gather_digests(local, total, DIGEST_BYTES)
+        torch.cuda.synchronize()
+        gather_seconds = max_over_ranks(time.perf_counter() - t0)
+        gathered_sum = int(everything.view(torch.int64).sum().item()) & (2**64 - 1)
+        gather = {"ms": gather_seconds * 1e3, "bytes_per_rank": total * DIGEST_BYTES,
+                  "checksum_matches": gathered_sum == checksum,
+                  "backend": "gloo (host tensors; validation only)" if args.share_gpu else "nccl"}
+        del everything, local
+
     # ---- end to end through the host-buffer C entry (pinned host memory) -----------
     e2e = None
     if not args.no_e2e:
@@ -599,6 +619,8 @@ def main():
         }
         if e2e:
             line["e2e"] = e2e
+        if gather:
+            line["digest_gather"] = gather
         if world == 1 and not args.no_dropin:
             dropin = dropin_cpp_wall()
             if dropin:

@@ -47,6 +47,35 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
+def gather_digests(local, total: int, digest_bytes: int):
+    """The optional step AFTER the hot path: every rank receives the digests
+    of the whole batch, in message order, from the contiguous shards of shard_range().
+    `local` is this rank's (count, digest_bytes) uint8 tensor -- on the GPU under NCCL (the
+    exchange then runs over NVLink), on the CPU under gloo.  One all_gather of equal-sized
+    blocks (shards differ by at most one message; the short ones are padded), then the padding
+    is cut out.  Nothing on the data path needs this: digests stay with their shard unless a
+    caller wants them in one place."""
+    import torch
+    import torch.distributed as dist
+    local = local.reshape(-1, digest_bytes)
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        assert local.shape[0] == total
+        return local
+    world, rank = dist.get_world_size(), dist.get_rank()
+    counts = [shard_range(total, r, world)[1] for r in range(world)]
+    assert local.shape[0] == counts[rank], "local digests do not match this rank's shard"
+    widest = max(counts)
+    block = local
+    if counts[rank] < widest:
+        block = torch.zeros((widest, digest_bytes), dtype=local.dtype, device=local.device)
+        block[:counts[rank]] = local
+    out = torch.empty((world, widest, digest_bytes), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out.view(-1), block.contiguous().view(-1))
+    if min(counts) == widest:
+        return out.view(total, digest_bytes)
+    return torch.cat([out[r, :counts[r]] for r in range(world)])
+
+
 def xor_fold_checksum(digest_bytes: np.ndarray) -> int:
     """Order-independent 64-bit checksum of a digest array: XOR of all 8-byte words.
     The XOR over ranks of per-rank values equals the single-GPU value."""

@@ -65,9 +65,12 @@ def _check_sharded(line, single, ranks):
 
 @pytest.mark.parametrize("ranks", [2, 4])
 def test_ranks_sharing_one_gpu_match_the_single_rank_run(single, ranks):
-    line = _bench(ranks, "--share-gpu")
+    line = _bench(ranks, "--share-gpu", "--gather-digests")
     assert "validation_only" in line
     _check_sharded(line, single, ranks)
+    # the optional gather after the hot path: every rank holds all digests, in message order
+    assert line["digest_gather"]["checksum_matches"] is True
+    assert line["digest_gather"]["bytes_per_rank"] == (1 << LOG2) * 32
 
 
 def test_nccl_branch_when_two_devices_are_visible(single):
@@ -75,6 +78,7 @@ def test_nccl_branch_when_two_devices_are_visible(single):
     if torch.cuda.device_count() < 2:
         pytest.skip("one CUDA device visible: the NCCL branch needs two (the gloo/shared-GPU test above "
                     "covers the same shard, barrier and reduction code)")
-    line = _bench(2)
+    line = _bench(2, "--gather-digests")
     assert "validation_only" not in line
     _check_sharded(line, single, 2)
+    assert line["digest_gather"]["checksum_matches"] is True and line["digest_gather"]["backend"] == "nccl"

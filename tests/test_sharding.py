@@ -103,6 +103,41 @@ def test_two_rank_gloo_run_matches_single_rank(oracle):
     assert [g[:2] for g in gathered] == [shard_range(total, r, world) for r in range(world)]
 
 
+def _gather_main(rank, world, port, total, out_queue):
+    import torch
+    import torch.distributed as dist
+    from oracle.binding import Oracle
+    from paper_1902_05320_b200.sharding import gather_digests
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    first, count = shard_range(total, rank, world)
+    data = workload_slice(total * 64, 64, first, count, seed=1)
+    local = torch.from_numpy(Oracle().hash_batch(1, data, fixed_len=64, count=count).reshape(count, 32).copy())
+    everything = gather_digests(local, total, 32)
+    out_queue.put((rank, everything.numpy().tobytes()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total,world", [(20_001, 2), (1_000, 3)])
+def test_gathered_digests_are_the_unsharded_result(oracle, total, world):
+    """After-the-fact digest gather (optional): every rank ends up with the
+    digests of the whole batch in message order, uneven shards included."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_main, args=(r, world, port, total, q)) for r in range(world)]
+    [p.start() for p in procs]
+    got = dict(q.get(timeout=120) for _ in range(world))
+    [p.join(timeout=60) for p in procs]
+    assert all(p.exitcode == 0 for p in procs)
+    whole = oracle.hash_batch(1, oracle.generate_workload(total * 64, 64, seed=1), fixed_len=64, count=total)
+    for rank in range(world):
+        assert got[rank] == whole.tobytes()
+
+
 def test_shard_properties_hypothesis():
     """Property form of the partition tests of proj/tests/test_batch.cpp:51-70: ranges are
     contiguous, disjoint and cover the batch, for any batch shape and GPU count."""
