@@ -409,7 +409,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1902_05320_b200 import Engine
+    from paper_1902_05320_b200 import Engine, library_info
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -589,6 +589,7 @@ def main():
                        "kernel": kernel_name + " (UNROLL 23 = peeled 1 + 7x3 + 2 rounds, ALU only)"},
             "gb_per_s_hashed": value * MSG_LEN / 1e9,
             "gpu_launches": launches,
+            "library": library_info(),
             "digest_checksum": f"{checksum:016x}",
             "clocks": clocks,
             "roofline": {

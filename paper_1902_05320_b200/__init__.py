@@ -10,5 +10,5 @@ There is no CPU fallback: importing ``engine`` without the built library, or
 calling it without a CUDA device, raises.
 """
 from .engine import (ALGORITHMS, BatchHasher, Engine, EngineError, EngineStateError,  # noqa: F401
-                     algorithm_id, digest_bytes, library_path, permutations, rate_bytes,
+                     algorithm_id, digest_bytes, library_info, library_path, permutations, rate_bytes,
                      selected_kernel)

@@ -53,6 +53,18 @@ def library_path() -> pathlib.Path:
     return _LIB_PATH
 
 
+def library_info() -> dict:
+    """Provenance of the loaded library for reports: path, version string (compiler and build
+    time, from the library itself), size, modification time and a CRC-32 of the file."""
+    import time
+    import zlib
+    raw = _LIB_PATH.read_bytes()
+    stat = _LIB_PATH.stat()
+    return {"path": str(_LIB_PATH), "version": _library().b200sha3_version().decode(), "bytes": len(raw),
+            "mtime_utc": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime(stat.st_mtime)),
+            "crc32": f"{zlib.crc32(raw):08x}"}
+
+
 def algorithm_id(algorithm) -> int:
     if isinstance(algorithm, str):
         name = algorithm.lower().replace("-", "_")

@@ -50,3 +50,5 @@ def test_bench_line_shape_at_reduced_size():
     if base["kind"] == "reference":
         assert set(base["builds_hashes_per_s"]) <= {"as_shipped", "hash_into"} and base["build"] in base["builds_hashes_per_s"]
     assert set(line["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    # build provenance of the library that ran
+    assert "sm_100a" in line["library"]["version"] and line["library"]["path"].endswith("libb200sha3.so")
