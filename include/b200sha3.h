@@ -100,9 +100,12 @@ enum {
   B200SHA3_KERNEL_WARP = 5,      /* one message per warp (25 lanes over 25 threads,
                                     shuffles): AUTO picks it for batches of few
                                     multi-block messages                           */
-  B200SHA3_KERNEL_PAIR = 6       /* one message per pair of threads (low / high halves
+  B200SHA3_KERNEL_PAIR = 6,      /* one message per pair of threads (low / high halves
                                     of every lane, one shuffle per rotation): kept
                                     for the measured comparison, never AUTO         */
+  B200SHA3_KERNEL_FEWBLOCK = 7   /* equal-length multi-block shapes with a static
+                                    shape (cfg2 / cfg3 lengths): AUTO picks it when
+                                    an instantiation fits                            */
 };
 
 /* Optional per-call configuration; NULL means all defaults.  The analogue of

@@ -95,13 +95,18 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
   const bool whole_bytes = args.last_mask == 0xffu;
   const bool fits_oneblock = whole_bytes && oneblock_supported(v.rate_lanes, msg_len, digest_bytes) &&
                              is_aligned(d_data, 16) && is_aligned(d_digests, 16);
+  // multi-block shapes of cfg2 / cfg3 with a static-shape instantiation (kernel_fewblock.cu)
+  const bool fits_fewblock = whole_bytes && fewblock_supported(v.rate_lanes, msg_len, digest_bytes) &&
+                             is_aligned(d_data, 16) && is_aligned(d_digests, 16);
   // single-block lengths the one-block kernel has no shape for (10, 20, 100 bytes ...)
-  const bool fits_short = !fits_oneblock && c.kernel == B200SHA3_KERNEL_AUTO &&
+  const bool fits_short = !fits_oneblock && !fits_fewblock && c.kernel == B200SHA3_KERNEL_AUTO &&
                           msg_len < 8u * static_cast<uint64_t>(v.rate_lanes) &&
                           args.last_mask == 0xffu && short_supported(v.rate_lanes, digest_bytes);
   int kernel = c.kernel;
   if (kernel == B200SHA3_KERNEL_AUTO) {
-    kernel = fits_oneblock ? B200SHA3_KERNEL_ONEBLOCK : B200SHA3_KERNEL_GENERIC;
+    kernel = fits_oneblock   ? B200SHA3_KERNEL_ONEBLOCK
+             : fits_fewblock ? B200SHA3_KERNEL_FEWBLOCK
+                             : B200SHA3_KERNEL_GENERIC;
     // few multi-block messages: latency of the sponge chain is all there is
     if (count <= warp_kernel_max_count() && (c.flags & B200SHA3_FLAG_NO_WARP_KERNEL) == 0 &&
         b200sha3_permutations(algorithm, msg_len, xof_bits) >= 2) {
@@ -124,6 +129,13 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
     plan.fma_preset = c.fma_preset >= 0 ? c.fma_preset : kDefaultFmaOneblock;
     args.aligned8 = 1u;
     err = launch_hash_oneblock(args, plan, stream);
+  } else if (kernel == B200SHA3_KERNEL_FEWBLOCK) {
+    if (!fits_fewblock) {
+      set_error_text("few-block kernel has no instantiation for this batch");
+      return B200SHA3_ERR_UNSUPPORTED;
+    }
+    args.aligned8 = 1u;
+    err = launch_hash_fewblock(args, plan, stream);
   } else if (kernel == B200SHA3_KERNEL_LANESPLIT) {
     if (!whole_bytes || !lanesplit_supported(v.rate_lanes, msg_len, digest_bytes) || !args.aligned8) {
       set_error_text("lane-split kernel does not fit this batch");
@@ -319,6 +331,9 @@ const char* b200sha3_selected_kernel(int algorithm, uint64_t msg_len, uint64_t c
     }
   } else if (whole_bytes && oneblock_supported(v.rate_lanes, msg_len, digest_bytes)) {  // run_fixed_slice
     std::snprintf(name, sizeof name, "hash_oneblock_kernel<%d,%d,%d>", v.rate_lanes,
+                  static_cast<int>(msg_len / 8), static_cast<int>(digest_bytes / 4));
+  } else if (whole_bytes && fewblock_supported(v.rate_lanes, msg_len, digest_bytes)) {
+    std::snprintf(name, sizeof name, "hash_fewblock_kernel<%d,%d,%d>", v.rate_lanes,
                   static_cast<int>(msg_len / 8), static_cast<int>(digest_bytes / 4));
   } else if (whole_bytes && msg_len < 8u * static_cast<uint64_t>(v.rate_lanes) &&
              short_supported(v.rate_lanes, digest_bytes)) {

@@ -1,0 +1,185 @@
+// kernel_fewblock.cu -- equal-length MULTI-block shapes (cfg2 lengths at or above the rate, cfg3
+// outputs longer than the rate), one message per thread, everything about the shape static.
+//
+// hash_into (proj/core/src/batch.cpp:15-25) for a batch whose messages are ML whole lanes and whose
+// digests are OW whole 32-bit words, both compile-time: NB = ML / RL full blocks are absorbed
+// (sponge.cpp:87-110), then the REM = ML % RL remaining lanes with the pad (sponge.cpp:113-129), then
+// NS - 1 more permutations between the NS output blocks (sponge.cpp:131-143) -- P = NB + NS
+// permutations per message.  The generic kernel runs these shapes at 0.985-0.99 of the ALU
+// roofline: nothing stalls, it just carries instructions a static shape does not need (offsets,
+// lengths, jump tables over the tail and the digest size, a permutation that cannot drop dead
+// work).  Here the 24 P rounds of a message are ONE sequence
+//
+//     round 0 | (8 P - 1) x [3 rounds] | rounds 22, 23 of the last permutation
+//
+// with the first round and the last two straight-line (ptxas drops the work on the capacity
+// lanes, zero before the first permutation, and on the lanes nobody reads after the last one,
+// as in the one-block kernel) and ONE rolled copy of three rounds in between, ~17 KB of code in
+// all.  What happens BETWEEN permutations -- absorb the next block, absorb the final block and
+// pad, or store an output block -- sits in front of the third round of every eighth loop body
+// (that round is round 0 of the next permutation), behind a warp-uniform branch; lane indices
+// are static everywhere, only the block's base pointer is a run-time value.
+#include "kernels.cuh"
+#include "sponge.cuh"
+
+namespace b200sha3 {
+
+namespace {
+
+// iota constants as (lo, hi) pairs, keccak.cpp:34-43, with round 0 repeated at index 24: the
+// loop body starting at round 22 ends with round 0 of the next permutation.
+__constant__ uint32_t kRoundConstWrap[50] = {
+    0x00000001u, 0x00000000u, 0x00008082u, 0x00000000u, 0x0000808au, 0x80000000u,
+    0x80008000u, 0x80000000u, 0x0000808bu, 0x00000000u, 0x80000001u, 0x00000000u,
+    0x80008081u, 0x80000000u, 0x00008009u, 0x80000000u, 0x0000008au, 0x00000000u,
+    0x00000088u, 0x00000000u, 0x80008009u, 0x00000000u, 0x8000000au, 0x00000000u,
+    0x8000808bu, 0x00000000u, 0x0000008bu, 0x80000000u, 0x00008089u, 0x80000000u,
+    0x00008003u, 0x80000000u, 0x00008002u, 0x80000000u, 0x00000080u, 0x80000000u,
+    0x0000800au, 0x00000000u, 0x8000000au, 0x80000000u, 0x80008081u, 0x80000000u,
+    0x00008080u, 0x80000000u, 0x80000001u, 0x00000000u, 0x80008008u, 0x80000000u,
+    0x00000001u, 0x00000000u};
+
+// Stores the first N lanes of the state to w (8-byte aligned) with 16-byte stores where w
+// allows: half the store instructions and half the sector writes of 8-byte ones (a thread's
+// output blocks are 256 or 512 bytes apart from its neighbour's, so nothing coalesces across
+// threads).  `off8`: w is 8 bytes past a 16-byte boundary (kernel-uniform).
+template <int N>
+__device__ __forceinline__ void store_lanes(const State& a, uint8_t* w, bool off8) {
+  if (!off8) {
+#pragma unroll
+    for (int j = 0; j + 1 < N; j += 2) {
+      __stcs(reinterpret_cast<uint4*>(w + 8 * j), make_uint4(a.lo[j], a.hi[j], a.lo[j + 1], a.hi[j + 1]));
+    }
+    if (N % 2 != 0) __stcs(reinterpret_cast<uint2*>(w + 8 * (N - 1)), make_uint2(a.lo[N - 1], a.hi[N - 1]));
+  } else {
+    __stcs(reinterpret_cast<uint2*>(w), make_uint2(a.lo[0], a.hi[0]));
+#pragma unroll
+    for (int j = 1; j + 1 < N; j += 2) {
+      __stcs(reinterpret_cast<uint4*>(w + 8 * j), make_uint4(a.lo[j], a.hi[j], a.lo[j + 1], a.hi[j + 1]));
+    }
+    if (N % 2 == 0) __stcs(reinterpret_cast<uint2*>(w + 8 * (N - 1)), make_uint2(a.lo[N - 1], a.hi[N - 1]));
+  }
+}
+
+template <int RL, int ML, int OW>
+__global__ void __launch_bounds__(256)
+hash_fewblock_kernel(const uint8_t* __restrict__ data, uint8_t* __restrict__ digests, uint64_t count,
+                     uint32_t head) {
+  constexpr int NB = ML / RL;                       // whole blocks absorbed before the final one
+  constexpr int REM = ML % RL;                      // message lanes of the final block
+  constexpr int NS = (OW + 2 * RL - 1) / (2 * RL);  // output blocks
+  constexpr int P = NB + NS;                        // permutations per message
+  constexpr int LAST_W = OW - (NS - 1) * 2 * RL;    // 32-bit words of the last output block
+  static_assert(P >= 2, "single-permutation shapes belong to the one-block kernel");
+  static_assert(NS == 1 || OW % 4 == 0, "output blocks are stored with 16-byte stores into 16-byte aligned slots");
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (tid >= count) return;
+  const uint2* q = reinterpret_cast<const uint2*>(data + tid * (8ull * ML));
+  uint8_t* o = digests + tid * (4ull * OW);
+
+  State a;
+  state_zero(a);
+  // in front of permutation 0: the first block, whole (NB >= 1) or final
+#pragma unroll
+  for (int j = 0; j < (NB >= 1 ? RL : REM); ++j) {
+    const uint2 v = __ldg(q + j);
+    a.lo[j] = v.x;
+    a.hi[j] = v.y;
+  }
+  if constexpr (NB == 0) {
+    a.lo[REM] ^= head;             // sponge.cpp:122-123
+    a.hi[RL - 1] ^= 0x80000000u;   // sponge.cpp:124-125
+  }
+  keccak_round<0u>(a, static_cast<uint32_t>(round_constant(0)), static_cast<uint32_t>(round_constant(0) >> 32));
+
+  uint32_t r = 1u;  // round number of the loop body's first round
+  int k = 0;        // permutations started so far, minus one
+#pragma unroll 1
+  for (int i = 0; i < 8 * P - 1; ++i) {
+    keccak_round<0u>(a, kRoundConstWrap[2u * r], kRoundConstWrap[2u * r + 1u]);
+    keccak_round<0u>(a, kRoundConstWrap[2u * r + 2u], kRoundConstWrap[2u * r + 3u]);
+    if (r == 22u) {  // permutation k is complete after these two rounds; the next round starts k + 1
+      ++k;
+      if (NB >= 2 && k < NB) {  // whole block k
+        const uint2* b = q + k * RL;
+#pragma unroll
+        for (int j = 0; j < RL; ++j) {
+          const uint2 v = __ldg(b + j);
+          a.lo[j] ^= v.x;
+          a.hi[j] ^= v.y;
+        }
+      } else if (NB >= 1 && k == NB) {  // final block: REM lanes, pad
+        const uint2* b = q + NB * RL;
+#pragma unroll
+        for (int j = 0; j < REM; ++j) {
+          const uint2 v = __ldg(b + j);
+          a.lo[j] ^= v.x;
+          a.hi[j] ^= v.y;
+        }
+        a.lo[REM] ^= head;
+        a.hi[RL - 1] ^= 0x80000000u;
+      } else if (NS >= 2) {  // output block k - NB - 1 is complete
+        // the digest slot is 16-byte aligned and a block is 8 RL bytes: with RL odd every other
+        // block starts 8 bytes off
+        const uint32_t m = static_cast<uint32_t>(k - NB - 1);
+        store_lanes<RL>(a, o + m * (8u * RL), RL % 2 != 0 && (m & 1u) != 0u);
+      }
+    }
+    keccak_round<0u>(a, kRoundConstWrap[2u * r + 4u], kRoundConstWrap[2u * r + 5u]);
+    r = r == 22u ? 1u : r + 3u;
+  }
+  keccak_round<0u>(a, static_cast<uint32_t>(round_constant(22)), static_cast<uint32_t>(round_constant(22) >> 32));
+  keccak_round<0u>(a, static_cast<uint32_t>(round_constant(23)), static_cast<uint32_t>(round_constant(23) >> 32));
+  if constexpr (NS == 1) {
+    emit_words_static<RL, LAST_W, OW % 4 == 0>(a, o);
+  } else {  // LAST_W is even here (OW % 4 == 0, whole lanes before it)
+    store_lanes<LAST_W / 2>(a, o + (NS - 1) * (8 * RL), ((NS - 1) * 8 * RL) % 16 != 0);
+  }
+}
+
+// (rate lanes, message lanes, output 32-bit words)
+#define B200SHA3_FEWBLOCK_SHAPES(X)                                                               \
+  X(18, 32, 7) X(18, 64, 7) X(18, 128, 7)                /* SHA3-224: 256 / 512 / 1024 B       */ \
+  X(17, 32, 8) X(17, 64, 8) X(17, 128, 8)                /* SHA3-256: 256 / 512 / 1024 B       */ \
+  X(13, 16, 12) X(13, 32, 12) X(13, 64, 12) X(13, 128, 12) /* SHA3-384: 128 ... 1024 B         */ \
+  X(9, 16, 16) X(9, 32, 16) X(9, 64, 16) X(9, 128, 16)   /* SHA3-512: 128 ... 1024 B           */ \
+  X(21, 8, 64) X(21, 8, 128)                             /* SHAKE128: 64 B -> 2048 / 4096 bits */ \
+  X(17, 8, 64) X(17, 8, 128)                             /* SHAKE256: 64 B -> 2048 / 4096 bits */
+
+}  // namespace
+
+bool fewblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes) {
+  if (msg_len % 8 != 0 || digest_bytes % 4 != 0 || msg_len > 1024 || digest_bytes > 512) return false;
+  const int ml = static_cast<int>(msg_len / 8), ow = static_cast<int>(digest_bytes / 4);
+#define X(RL, ML, OW) \
+  if (rate_lanes == RL && ml == ML && ow == OW) return true;
+  B200SHA3_FEWBLOCK_SHAPES(X)
+#undef X
+  return false;
+}
+
+// Equal-length, 16-byte aligned data and digests, whole-byte output (no XOF tail mask).
+cudaError_t launch_hash_fewblock(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {
+  if (!fewblock_supported(plan.rate_lanes, args.fixed_len, args.digest_bytes) || args.offsets || args.lengths ||
+      args.order || !args.aligned8 || args.last_mask != 0xffu) {
+    return cudaErrorNotSupported;
+  }
+  // 128 threads per block; 256 measured 0.3 % faster for the SHAKE128 shapes (and slower for
+  // the others): tools/fewblock_sweep.py
+  const int threads = plan.block_threads > 0 ? plan.block_threads : plan.rate_lanes == 21 ? 256 : 128;
+  const uint64_t blocks = (args.count + threads - 1) / threads;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+  const int ml = static_cast<int>(args.fixed_len / 8), ow = static_cast<int>(args.digest_bytes / 4);
+#define X(RL, ML, OW)                                                                              \
+  if (plan.rate_lanes == RL && ml == ML && ow == OW) {                                             \
+    hash_fewblock_kernel<RL, ML, OW><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(       \
+        args.data, args.digests, args.count, args.head);                                           \
+    return cudaGetLastError();                                                                     \
+  }
+  B200SHA3_FEWBLOCK_SHAPES(X)
+#undef X
+  return cudaErrorNotSupported;
+}
+
+}  // namespace b200sha3

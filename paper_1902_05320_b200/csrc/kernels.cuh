@@ -68,6 +68,12 @@ cudaError_t launch_hash_oneblock(const HashArgs& args, const LaunchPlan& plan,
                                  cudaStream_t stream);
 bool oneblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
 
+// Equal-length multi-block shapes with everything static (kernel_fewblock.cu): messages of whole
+// lanes at or above the rate, or outputs longer than the rate, for the shapes of BASELINE.json
+// cfg2 / cfg3; 16-byte aligned buffers, whole-byte output.  cudaErrorNotSupported otherwise.
+cudaError_t launch_hash_fewblock(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
+bool fewblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
+
 // Variable-length batches made of single-block messages only (kernel_short.cu), input order; for
 // callers that KNOW the batch is all-short (the host entries).  Returns at once if the "long" flag
 // word says otherwise.  cudaErrorNotSupported when no instantiation matches.

@@ -28,6 +28,7 @@ _LIB_PATH = _HERE / "libb200sha3.so"
 OK, ERR_INVALID_ARGUMENT, ERR_CUDA, ERR_UNSUPPORTED, ERR_STATE = 0, 1, 2, 3, 4
 FLAG_NO_BUCKETING, FLAG_NO_PIPELINE, FLAG_NO_WARP_KERNEL = 1, 2, 4
 KERNEL_AUTO, KERNEL_GENERIC, KERNEL_ONEBLOCK, KERNEL_LANESPLIT, KERNEL_STAGED, KERNEL_WARP, KERNEL_PAIR = 0, 1, 2, 3, 4, 5, 6
+KERNEL_FEWBLOCK = 7
 
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)

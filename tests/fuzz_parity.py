@@ -63,11 +63,16 @@ def main():
         no_warp = FLAG_NO_WARP_KERNEL if rng.random() < 0.5 else 0
         if entry.startswith("fixed"):
             n = int(lengths[0])
+            if rng.random() < 0.35:  # the static multi-block shapes (kernel_fewblock.cu) and their neighbours
+                n = int(rng.choice([128, 256, 512, 1024])) if alg < 4 else 64
+                bits = 0 if alg < 4 else int(rng.choice([2048, 4096, 2045]))
+                n += int(rng.choice([0, 0, 0, 8, -8]))
+                entry += "_shape"
             fixed = rng.integers(0, 256, max(count * n, 1) + 16, dtype=np.uint8)
             expect = oracle.hash_batch(alg, fixed, fixed_len=n, count=count, xof_bits=bits, workers=8)
             kernel = int(rng.choice([KERNEL_AUTO, KERNEL_AUTO, KERNEL_GENERIC, KERNEL_STAGED, KERNEL_WARP, KERNEL_PAIR]))
             eng = Engine(kernel=kernel, flags=no_warp)
-            if entry == "fixed_device":
+            if entry.startswith("fixed_device"):
                 got = eng.hash_fixed(alg, torch.from_numpy(fixed).cuda(), n, count, bits).cpu().numpy()
             else:
                 got = eng.hash_fixed(alg, fixed, n, count, bits)

@@ -155,7 +155,9 @@ def test_selected_kernel_names():
     from paper_1902_05320_b200 import selected_kernel
     assert selected_kernel("sha3_256", 64) == "hash_oneblock_kernel<17,8,8>"
     assert selected_kernel("sha3_256", 10) == "hash_short_fixed_kernel<17,8>"
-    assert selected_kernel("sha3_512", 1024) == "hash_generic_kernel<9>"
+    assert selected_kernel("sha3_512", 1024) == "hash_fewblock_kernel<9,128,16>"  # static multi-block shape
+    assert selected_kernel("sha3_512", 1032) == "hash_generic_kernel<9>"
+    assert selected_kernel("shake256", 64, 4096) == "hash_fewblock_kernel<17,8,128>"
     assert selected_kernel("shake128", 64, 1023) == "hash_generic_kernel<21>"     # odd bits: masked tail
     assert selected_kernel("shake128", 64, 1024) == "hash_oneblock_kernel<21,8,32>"
     assert selected_kernel("sha3_256", None) == "bucket_order + hash_ragged_kernel<17,8>"

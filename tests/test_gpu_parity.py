@@ -238,6 +238,49 @@ def test_oneblock_shapes(oracle, algorithm, msg_len, bits):
         Engine(kernel=KERNEL_ONEBLOCK).hash_fixed(algorithm, dev[:count * 24].contiguous(), 24, count, bits)
 
 
+FEWBLOCK_SHAPES = ([(0, n, 0) for n in (256, 512, 1024)] + [(1, n, 0) for n in (256, 512, 1024)] +
+                   [(2, n, 0) for n in (128, 256, 512, 1024)] + [(3, n, 0) for n in (128, 256, 512, 1024)] +
+                   [(4, 64, 2048), (4, 64, 4096), (5, 64, 2048), (5, 64, 4096)])
+
+
+@pytest.mark.parametrize("algorithm,msg_len,bits", FEWBLOCK_SHAPES)
+def test_fewblock_shapes(oracle, algorithm, msg_len, bits):
+    """Every instantiated shape of the static-shape multi-block kernel (kernel_fewblock.cu),
+    forced, vs the oracle and vs the generic kernel; KERNEL_AUTO picks it for large batches of
+    these shapes; shapes without an instantiation, odd-bit XOF lengths and misaligned buffers
+    are refused when forced (and served by the generic kernel under AUTO)."""
+    import torch
+    from paper_1902_05320_b200 import Engine, EngineError, selected_kernel
+    from paper_1902_05320_b200.engine import FLAG_NO_WARP_KERNEL, KERNEL_FEWBLOCK, KERNEL_GENERIC
+    count = 4099
+    host = oracle.generate_workload(count * msg_len, msg_len, seed=23)
+    dev = torch.from_numpy(host).cuda()
+    expect = oracle.hash_batch(algorithm, host, fixed_len=msg_len, count=count, xof_bits=bits, workers=4)
+    forced = Engine(kernel=KERNEL_FEWBLOCK)
+    got = forced.hash_fixed(algorithm, dev, msg_len, count, bits)
+    assert (got.cpu().numpy() == expect).all()
+    assert torch.equal(got, Engine(kernel=KERNEL_GENERIC).hash_fixed(algorithm, dev, msg_len, count, bits))
+    assert selected_kernel(algorithm, msg_len, bits, 1 << 20).startswith("hash_fewblock_kernel<")
+    auto = Engine(flags=FLAG_NO_WARP_KERNEL)
+    assert torch.equal(got, auto.hash_fixed(algorithm, dev, msg_len, count, bits))
+    # one message, and a count that leaves the last block of threads almost empty
+    for n in (1, 129):
+        assert (forced.hash_fixed(algorithm, dev, msg_len, n, bits).cpu().numpy() == expect[:n]).all()
+    with pytest.raises(EngineError):  # no such shape
+        forced.hash_fixed(algorithm, dev[:count * (msg_len - 8)].contiguous(), msg_len - 8, count, bits)
+    # a buffer that is only 8-byte aligned: refused when forced, the generic kernel under AUTO
+    shifted = torch.empty(host.size + 8, dtype=torch.uint8, device="cuda")[8:]
+    shifted.copy_(dev)
+    with pytest.raises(EngineError):
+        forced.hash_fixed(algorithm, shifted, msg_len, count, bits)
+    assert (auto.hash_fixed(algorithm, shifted, msg_len, count, bits).cpu().numpy() == expect).all()
+    if bits:  # an XOF length that rounds up to the same digest size but is not whole bytes
+        with pytest.raises(EngineError):
+            forced.hash_fixed(algorithm, dev, msg_len, count, bits - 3)
+        odd = oracle.hash_batch(algorithm, host, fixed_len=msg_len, count=count, xof_bits=bits - 3, workers=4)
+        assert (auto.hash_fixed(algorithm, dev, msg_len, count, bits - 3).cpu().numpy() == odd).all()
+
+
 @pytest.mark.parametrize("algorithm", [4, 5])
 @pytest.mark.parametrize("msg_len", [32, 64, 128])
 @pytest.mark.parametrize("bits", [250, 255, 509, 1023])

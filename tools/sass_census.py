@@ -91,6 +91,48 @@ def census(instrs, trip_count=None):
     return rec
 
 
+def census_fewblock(instrs, rl, ml, ow):
+    """hash_fewblock_kernel<RL, ML, OW>: head (round 0) + (8 P - 1) x [3 rounds] + tail (rounds 22,
+    23 of the last permutation), P = ML / RL + ceil(OW / 2 RL); the code between two
+    permutations (absorb XORs / output stores) sits inside the loop behind a forward branch and
+    runs once per permutation boundary.  Executed LOP3+SHF per message = head + trips x (loop
+    body outside that section) + tail + the absorb XORs of the blocks after the first."""
+    rec = census(instrs)
+    nb, rem = ml // rl, ml % rl
+    perms = nb + -(-ow // (2 * rl))
+    back = []
+    for addr, op, rest in instrs:
+        if op.startswith("BRA"):
+            m = BRANCH_TARGET.search(rest)
+            if m and int(m.group(1), 16) < addr:
+                back.append((int(m.group(1), 16), addr))
+    if len(back) != 1:
+        return rec
+    lo, hi = back[0]
+    # the forward branch inside the loop that skips the between-permutations section
+    skip = None
+    for addr, op, rest in instrs:
+        if lo <= addr <= hi and op.startswith("BRA"):
+            m = BRANCH_TARGET.search(rest)
+            if m and addr < int(m.group(1), 16) <= hi:
+                skip = (addr, int(m.group(1), 16))
+                break
+    if not skip:
+        return rec
+    alu = lambda op: op.split(".")[0] in ("LOP3", "SHF")
+    head = sum(alu(op) for a, op, _ in instrs if a < lo)
+    body = sum(alu(op) for a, op, _ in instrs if lo <= a <= hi and not (skip[0] < a < skip[1]))
+    exit_addr = max(a for a, op, _ in instrs if op.startswith("EXIT"))
+    tail = sum(alu(op) for a, op, _ in instrs if hi < a <= exit_addr)
+    absorb = (2 * rl * (nb - 1) if nb >= 2 else 0) + (2 * rem + 2 if nb >= 1 else 0)
+    trips = 8 * perms - 1
+    total = head + trips * body + tail + absorb
+    rec["executed_per_thread"] = {"LOP3+SHF": total, "permutations": perms, "LOP3+SHF per permutation": round(total / perms, 1),
+                                  "head": head, "loop_body": body, "loop_trip_count": trips, "tail": tail,
+                                  "absorb_xors_after_first_block": absorb}
+    return rec
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--lib", default=str(ROOT / "paper_1902_05320_b200" / "libb200sha3.so"))
@@ -114,6 +156,9 @@ def main():
         if m:
             trip = ONEBLOCK_LOOPS.get(int(m.group(4)))
         rec = census(instrs, trip)
+        m = re.match(r"hash_fewblock_kernel<(\d+), (\d+), (\d+)>", name)
+        if m:
+            rec = census_fewblock(instrs, int(m.group(1)), int(m.group(2)), int(m.group(3)))
         out[name] = rec
         rows.append((name, rec))
     pathlib.Path(args.json).write_text(json.dumps(out, indent=1) + "\n")
@@ -122,7 +167,8 @@ def main():
             "Generated by `python tools/sass_census.py` from `cuobjdump -sass "
             "paper_1902_05320_b200/libb200sha3.so` (nvcc 12.9, `-gencode arch=compute_100a,code=sm_100a -O3`).",
             "Static = instructions in the code object; executed = per thread per hash, the round-loop body "
-            "weighted by its trip count (only for kernels with a single loop, i.e. the one-block family). "
+            "weighted by its trip count (only for kernels with a single loop, i.e. the one-block family; for the "
+            "few-block family per MESSAGE, with the per-permutation figure in brackets). "
             "The contract figure of SURVEY.md 8(d) is 4320 LOP3+SHF per permutation; the headline kernel "
             "executes fewer because ptxas drops work on lanes that are zero entering round 0 and lanes nobody "
             "reads after round 23.", "",
@@ -134,7 +180,10 @@ def main():
         luts = " ".join(f"{k}:{v}" for k, v in rec["lop3_luts"].items())
         ex = rec.get("executed_per_thread")
         cells = [name, rec["static"]["LOP3"], rec["static"]["SHF"], rec["static"]["total"], luts]
-        cells += [ex["LOP3"], ex["SHF"], ex["LOP3+SHF"], ex["total"]] if ex else ["", "", "", ""]
+        if ex and "permutations" in ex:   # few-block family: per message, and per permutation in brackets
+            cells += ["", "", f'{ex["LOP3+SHF"]} ({ex["LOP3+SHF per permutation"]} x {ex["permutations"]})', ""]
+        else:
+            cells += [ex["LOP3"], ex["SHF"], ex["LOP3+SHF"], ex["total"]] if ex else ["", "", "", ""]
         head.append("| " + " | ".join(str(c) for c in cells) + " |")
     head += ["", "LUT legend: 0x96 = a^b^c (theta parities, theta apply), 0xd2 = a^(~b&c) (chi), 0x3c/0x5a/0x66 = two-input "
              "xor (iota, pad bytes), 0xfc/0xf8/0xc0... = byte assembly and address arithmetic in the generic kernels.", ""]
