@@ -39,32 +39,65 @@ __constant__ uint32_t kRoundConstWrap[50] = {
     0x00008080u, 0x80000000u, 0x80000001u, 0x00000000u, 0x80008008u, 0x80000000u,
     0x00000001u, 0x00000000u};
 
-// Stores the first N lanes of the state to w (8-byte aligned) with 16-byte stores where w
-// allows: half the store instructions and half the sector writes of 8-byte ones (a thread's
+// How an output block leaves the registers.  The vector stores need aligned register pairs /
+// quads, and WHERE ptxas then keeps the state decides how many LOP3 / SHF of the round loop read
+// three registers of one bank: 0-11 of 540 in a good allocation, 65-87 in a bad one, which runs
+// 1.5-2 % under its instruction count (tools/sass_bank_census.py counts them from the SASS;
+// hash_fewblock_kernel<21, 8, 128>: 87 -> 0.989 of the ALU roofline, 1 -> 1.006).  Stored straight
+// from the state, the quads of a 21-lane block pin the whole state into such an allocation
+// (87); stored from copies ptxas cannot coalesce (IMAD by a run-time 1: FMA pipe, next to
+// free), the state is unconstrained and lands in another bad one (79).  Copying SOME lanes
+// breaks the pattern: kCopyLanes was found by a search over random lane sets with that census
+// (most sets give <= 2; this one gives 0 for all four multi-block-output shapes).
+constexpr uint32_t kCopyLanes = 0x10b417u;  // lanes 0,1,2,4,10,12,13,15,20
+#ifdef B200SHA3_FEWBLOCK_COPY_MASK            // census / search builds
+#undef B200SHA3_FEWBLOCK_COPY_LANES
+#define B200SHA3_FEWBLOCK_COPY_LANES B200SHA3_FEWBLOCK_COPY_MASK
+#else
+#define B200SHA3_FEWBLOCK_COPY_LANES kCopyLanes
+#endif
+__device__ __forceinline__ uint32_t copy_reg(uint32_t v, uint32_t one) {
+  uint32_t t;
+  asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(t) : "r"(v), "r"(one));
+  return t;
+}
+// lane j of the state as (lo, hi), through copies if the lane is in the set (j is a
+// compile-time value after unrolling)
+__device__ __forceinline__ uint2 lane_out(const State& a, int j, uint32_t one) {
+  const bool c = ((B200SHA3_FEWBLOCK_COPY_LANES >> j) & 1u) != 0u;
+  return make_uint2(c ? copy_reg(a.lo[j], one) : a.lo[j], c ? copy_reg(a.hi[j], one) : a.hi[j]);
+}
+__device__ __forceinline__ void store2(uint8_t* w, const State& a, int j, uint32_t one) {
+  __stcs(reinterpret_cast<uint2*>(w), lane_out(a, j, one));
+}
+__device__ __forceinline__ void store4(uint8_t* w, const State& a, int j, uint32_t one) {
+  const uint2 u = lane_out(a, j, one), v = lane_out(a, j + 1, one);
+  __stcs(reinterpret_cast<uint4*>(w), make_uint4(u.x, u.y, v.x, v.y));
+}
+
+// Stores the first N lanes of the state to w (8-byte aligned) with 16-byte streaming stores where
+// w allows: half the store instructions and half the sector writes of 8-byte ones (a thread's
 // output blocks are 256 or 512 bytes apart from its neighbour's, so nothing coalesces across
-// threads).  `off8`: w is 8 bytes past a 16-byte boundary (kernel-uniform).
+// threads; 8-byte stores left the SHAKE256 shapes 1 % slower).  `off8`: w is 8 bytes past a
+// 16-byte boundary (kernel-uniform).
 template <int N>
-__device__ __forceinline__ void store_lanes(const State& a, uint8_t* w, bool off8) {
+__device__ __forceinline__ void store_lanes(const State& a, uint8_t* w, bool off8, uint32_t one) {
   if (!off8) {
 #pragma unroll
-    for (int j = 0; j + 1 < N; j += 2) {
-      __stcs(reinterpret_cast<uint4*>(w + 8 * j), make_uint4(a.lo[j], a.hi[j], a.lo[j + 1], a.hi[j + 1]));
-    }
-    if (N % 2 != 0) __stcs(reinterpret_cast<uint2*>(w + 8 * (N - 1)), make_uint2(a.lo[N - 1], a.hi[N - 1]));
+    for (int j = 0; j + 1 < N; j += 2) store4(w + 8 * j, a, j, one);
+    if (N % 2 != 0) store2(w + 8 * (N - 1), a, N - 1, one);
   } else {
-    __stcs(reinterpret_cast<uint2*>(w), make_uint2(a.lo[0], a.hi[0]));
+    store2(w, a, 0, one);
 #pragma unroll
-    for (int j = 1; j + 1 < N; j += 2) {
-      __stcs(reinterpret_cast<uint4*>(w + 8 * j), make_uint4(a.lo[j], a.hi[j], a.lo[j + 1], a.hi[j + 1]));
-    }
-    if (N % 2 == 0) __stcs(reinterpret_cast<uint2*>(w + 8 * (N - 1)), make_uint2(a.lo[N - 1], a.hi[N - 1]));
+    for (int j = 1; j + 1 < N; j += 2) store4(w + 8 * j, a, j, one);
+    if (N % 2 == 0) store2(w + 8 * (N - 1), a, N - 1, one);
   }
 }
 
 template <int RL, int ML, int OW>
 __global__ void __launch_bounds__(256)
 hash_fewblock_kernel(const uint8_t* __restrict__ data, uint8_t* __restrict__ digests, uint64_t count,
-                     uint32_t head) {
+                     uint32_t head, uint32_t one) {
   constexpr int NB = ML / RL;                       // whole blocks absorbed before the final one
   constexpr int REM = ML % RL;                      // message lanes of the final block
   constexpr int NS = (OW + 2 * RL - 1) / (2 * RL);  // output blocks
@@ -122,7 +155,7 @@ hash_fewblock_kernel(const uint8_t* __restrict__ data, uint8_t* __restrict__ dig
         // the digest slot is 16-byte aligned and a block is 8 RL bytes: with RL odd every other
         // block starts 8 bytes off
         const uint32_t m = static_cast<uint32_t>(k - NB - 1);
-        store_lanes<RL>(a, o + m * (8u * RL), RL % 2 != 0 && (m & 1u) != 0u);
+        store_lanes<RL>(a, o + m * (8u * RL), RL % 2 != 0 && (m & 1u) != 0u, one);
       }
     }
     keccak_round<0u>(a, kRoundConstWrap[2u * r + 4u], kRoundConstWrap[2u * r + 5u]);
@@ -133,10 +166,11 @@ hash_fewblock_kernel(const uint8_t* __restrict__ data, uint8_t* __restrict__ dig
   if constexpr (NS == 1) {
     emit_words_static<RL, LAST_W, OW % 4 == 0>(a, o);
   } else {  // LAST_W is even here (OW % 4 == 0, whole lanes before it)
-    store_lanes<LAST_W / 2>(a, o + (NS - 1) * (8 * RL), ((NS - 1) * 8 * RL) % 16 != 0);
+    store_lanes<LAST_W / 2>(a, o + (NS - 1) * (8 * RL), ((NS - 1) * 8 * RL) % 16 != 0, one);
   }
 }
 
+// (rate lanes, message lanes, output 32-bit words)
 // (rate lanes, message lanes, output 32-bit words)
 #define B200SHA3_FEWBLOCK_SHAPES(X)                                                               \
   X(18, 32, 7) X(18, 64, 7) X(18, 128, 7)                /* SHA3-224: 256 / 512 / 1024 B       */ \
@@ -164,9 +198,7 @@ cudaError_t launch_hash_fewblock(const HashArgs& args, const LaunchPlan& plan, c
       args.order || !args.aligned8 || args.last_mask != 0xffu) {
     return cudaErrorNotSupported;
   }
-  // 128 threads per block; 256 measured 0.3 % faster for the SHAKE128 shapes (and slower for
-  // the others): tools/fewblock_sweep.py
-  const int threads = plan.block_threads > 0 ? plan.block_threads : plan.rate_lanes == 21 ? 256 : 128;
+  const int threads = plan.block_threads > 0 ? plan.block_threads : 128;  // 64 / 128 / 256 swept: tools/fewblock_sweep.py
   const uint64_t blocks = (args.count + threads - 1) / threads;
   if (blocks == 0) return cudaSuccess;
   if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
@@ -174,7 +206,7 @@ cudaError_t launch_hash_fewblock(const HashArgs& args, const LaunchPlan& plan, c
 #define X(RL, ML, OW)                                                                              \
   if (plan.rate_lanes == RL && ml == ML && ow == OW) {                                             \
     hash_fewblock_kernel<RL, ML, OW><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(       \
-        args.data, args.digests, args.count, args.head);                                           \
+        args.data, args.digests, args.count, args.head, 1u);                                           \
     return cudaGetLastError();                                                                     \
   }
   B200SHA3_FEWBLOCK_SHAPES(X)
