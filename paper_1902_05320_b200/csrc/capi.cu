@@ -358,15 +358,6 @@ const char* b200sha3_strerror(int status) {
 
 const char* b200sha3_last_cuda_error(void) { return last_error_buffer(); }
 
-// Version + build provenance: which compiler produced the code object that is running and when
-// (a round summary can then tell a library rebuilt on the GPU box from one shipped with the tree).
-#define B200SHA3_STR2(x) #x
-#define B200SHA3_STR(x) B200SHA3_STR2(x)
-const char* b200sha3_version(void) {
-  return "b200sha3 0.2 (sm_100a; nvcc " B200SHA3_STR(__CUDACC_VER_MAJOR__) "." B200SHA3_STR(
-      __CUDACC_VER_MINOR__) "." B200SHA3_STR(__CUDACC_VER_BUILD__) "; built " __DATE__ " " __TIME__ ")";
-}
-
 int b200sha3_current_device(void) {
   int dev = -1;
   if (cudaGetDevice(&dev) != cudaSuccess) {
