@@ -103,9 +103,11 @@ enum {
   B200SHA3_KERNEL_PAIR = 6,      /* one message per pair of threads (low / high halves
                                     of every lane, one shuffle per rotation): kept
                                     for the measured comparison, never AUTO         */
-  B200SHA3_KERNEL_FEWBLOCK = 7   /* equal-length multi-block shapes with a static
-                                    shape (cfg2 / cfg3 lengths): AUTO picks it when
-                                    an instantiation fits                            */
+  B200SHA3_KERNEL_FEWBLOCK = 7   /* equal-length multi-block batches as one round
+                                    sequence per message: static-shape instantiations
+                                    (cfg2 / cfg3 lengths) or the run-time-length form
+                                    (any whole number of lanes at or above the rate);
+                                    AUTO picks it when one fits                       */
 };
 
 /* Optional per-call configuration; NULL means all defaults.  The analogue of

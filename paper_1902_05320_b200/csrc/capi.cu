@@ -96,8 +96,11 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
   const bool fits_oneblock = whole_bytes && oneblock_supported(v.rate_lanes, msg_len, digest_bytes) &&
                              is_aligned(d_data, 16) && is_aligned(d_digests, 16);
   // multi-block shapes of cfg2 / cfg3 with a static-shape instantiation (kernel_fewblock.cu)
-  const bool fits_fewblock = whole_bytes && fewblock_supported(v.rate_lanes, msg_len, digest_bytes) &&
-                             is_aligned(d_data, 16) && is_aligned(d_digests, 16);
+  const bool aligned16 = is_aligned(d_data, 16) && is_aligned(d_digests, 16);
+  const bool fits_static = whole_bytes && aligned16 && fewblock_supported(v.rate_lanes, msg_len, digest_bytes);
+  // ... or any other whole number of lanes at or above the rate, through the run-time-length form
+  const bool fits_fewblock = fits_static ||
+                             (whole_bytes && aligned16 && manyblock_supported(v.rate_lanes, msg_len, digest_bytes));
   // single-block lengths the one-block kernel has no shape for (10, 20, 100 bytes ...)
   const bool fits_short = !fits_oneblock && !fits_fewblock && c.kernel == B200SHA3_KERNEL_AUTO &&
                           msg_len < 8u * static_cast<uint64_t>(v.rate_lanes) &&
@@ -135,7 +138,7 @@ int run_fixed_slice(int algorithm, const uint8_t* d_data, uint64_t msg_len, uint
       return B200SHA3_ERR_UNSUPPORTED;
     }
     args.aligned8 = 1u;
-    err = launch_hash_fewblock(args, plan, stream);
+    err = fits_static ? launch_hash_fewblock(args, plan, stream) : launch_hash_manyblock(args, plan, stream);
   } else if (kernel == B200SHA3_KERNEL_LANESPLIT) {
     if (!whole_bytes || !lanesplit_supported(v.rate_lanes, msg_len, digest_bytes) || !args.aligned8) {
       set_error_text("lane-split kernel does not fit this batch");
@@ -335,6 +338,8 @@ const char* b200sha3_selected_kernel(int algorithm, uint64_t msg_len, uint64_t c
   } else if (whole_bytes && fewblock_supported(v.rate_lanes, msg_len, digest_bytes)) {
     std::snprintf(name, sizeof name, "hash_fewblock_kernel<%d,%d,%d>", v.rate_lanes,
                   static_cast<int>(msg_len / 8), static_cast<int>(digest_bytes / 4));
+  } else if (whole_bytes && manyblock_supported(v.rate_lanes, msg_len, digest_bytes)) {
+    std::snprintf(name, sizeof name, "hash_manyblock_kernel<%d,%d>", v.rate_lanes, static_cast<int>(digest_bytes / 4));
   } else if (whole_bytes && msg_len < 8u * static_cast<uint64_t>(v.rate_lanes) &&
              short_supported(v.rate_lanes, digest_bytes)) {
     std::snprintf(name, sizeof name, "hash_short_fixed_kernel<%d,%d>", v.rate_lanes,

@@ -171,6 +171,90 @@ hash_fewblock_kernel(const uint8_t* __restrict__ data, uint8_t* __restrict__ dig
 }
 
 // (rate lanes, message lanes, output 32-bit words)
+// The same round sequence with the message length a RUN-TIME value: equal-length messages of ANY
+// whole number of lanes at or above the rate (200-byte records, 1000-byte rows ...), digest of OW
+// words that fits one block.  nb = ml / RL whole blocks, then the final block of rem = ml % RL
+// lanes through a jump table over rem (kernel-uniform, every case static), so a message costs
+// the instructions of the static-shape kernel; only the zero-lane savings of round 0 need ml >= RL
+// (the first block is whole), which is this kernel's precondition.
+template <int RL, int REM>
+__device__ __forceinline__ void absorb_final_lanes(State& a, const uint2* b, uint32_t head) {
+#pragma unroll
+  for (int j = 0; j < REM; ++j) {
+    const uint2 v = __ldg(b + j);
+    a.lo[j] ^= v.x;
+    a.hi[j] ^= v.y;
+  }
+  a.lo[REM] ^= head;            // sponge.cpp:122-123
+  a.hi[RL - 1] ^= 0x80000000u;  // sponge.cpp:124-125
+}
+
+template <int RL, int OW>
+__global__ void __launch_bounds__(256)
+hash_manyblock_kernel(const uint8_t* __restrict__ data, uint8_t* __restrict__ digests, uint64_t count,
+                      uint32_t head, uint32_t ml) {
+  static_assert(OW <= 2 * RL, "digest must fit one block");
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (tid >= count) return;
+  const uint32_t nb = ml / RL, rem = ml - nb * RL;  // nb >= 1
+  const uint2* q = reinterpret_cast<const uint2*>(data + tid * (8ull * ml));
+  uint8_t* o = digests + tid * (4ull * OW);
+
+  State a;
+  state_zero(a);
+#pragma unroll
+  for (int j = 0; j < RL; ++j) {
+    const uint2 v = __ldg(q + j);
+    a.lo[j] = v.x;
+    a.hi[j] = v.y;
+  }
+  keccak_round<0u>(a, static_cast<uint32_t>(round_constant(0)), static_cast<uint32_t>(round_constant(0) >> 32));
+
+  uint32_t r = 1u, k = 0u;
+  const uint32_t trips = 8u * (nb + 1u) - 1u;
+#pragma unroll 1
+  for (uint32_t i = 0; i < trips; ++i) {
+    keccak_round<0u>(a, kRoundConstWrap[2u * r], kRoundConstWrap[2u * r + 1u]);
+    keccak_round<0u>(a, kRoundConstWrap[2u * r + 2u], kRoundConstWrap[2u * r + 3u]);
+    if (r == 22u) {
+      ++k;
+      const uint2* b = q + static_cast<uint64_t>(k) * RL;
+      if (k < nb) {  // whole block k
+#pragma unroll
+        for (int j = 0; j < RL; ++j) {
+          const uint2 v = __ldg(b + j);
+          a.lo[j] ^= v.x;
+          a.hi[j] ^= v.y;
+        }
+      } else {  // final block: rem lanes, pad
+        switch (rem) {
+#define B200SHA3_FINAL_CASE(R) \
+  case R:                      \
+    if constexpr (R < RL) absorb_final_lanes<RL, (R < RL ? R : 0)>(a, b, head); \
+    break;
+          B200SHA3_FINAL_CASE(0) B200SHA3_FINAL_CASE(1) B200SHA3_FINAL_CASE(2) B200SHA3_FINAL_CASE(3)
+          B200SHA3_FINAL_CASE(4) B200SHA3_FINAL_CASE(5) B200SHA3_FINAL_CASE(6) B200SHA3_FINAL_CASE(7)
+          B200SHA3_FINAL_CASE(8) B200SHA3_FINAL_CASE(9) B200SHA3_FINAL_CASE(10) B200SHA3_FINAL_CASE(11)
+          B200SHA3_FINAL_CASE(12) B200SHA3_FINAL_CASE(13) B200SHA3_FINAL_CASE(14) B200SHA3_FINAL_CASE(15)
+          B200SHA3_FINAL_CASE(16) B200SHA3_FINAL_CASE(17) B200SHA3_FINAL_CASE(18) B200SHA3_FINAL_CASE(19)
+          B200SHA3_FINAL_CASE(20)
+#undef B200SHA3_FINAL_CASE
+          default: break;
+        }
+      }
+    }
+    keccak_round<0u>(a, kRoundConstWrap[2u * r + 4u], kRoundConstWrap[2u * r + 5u]);
+    r = r == 22u ? 1u : r + 3u;
+  }
+  keccak_round<0u>(a, static_cast<uint32_t>(round_constant(22)), static_cast<uint32_t>(round_constant(22) >> 32));
+  keccak_round<0u>(a, static_cast<uint32_t>(round_constant(23)), static_cast<uint32_t>(round_constant(23) >> 32));
+  emit_words_static<RL, OW, OW % 4 == 0>(a, o);
+}
+
+// (rate lanes, output 32-bit words): the four hashes, the two SHAKEs at 128- / 256- / 512-bit outputs
+#define B200SHA3_MANYBLOCK_SHAPES(X) \
+  X(18, 7) X(17, 8) X(13, 12) X(9, 16) X(17, 4) X(17, 16) X(21, 4) X(21, 8) X(21, 16)
+
 // (rate lanes, message lanes, output 32-bit words)
 #define B200SHA3_FEWBLOCK_SHAPES(X)                                                               \
   X(18, 32, 7) X(18, 64, 7) X(18, 128, 7)                /* SHA3-224: 256 / 512 / 1024 B       */ \
@@ -210,6 +294,46 @@ cudaError_t launch_hash_fewblock(const HashArgs& args, const LaunchPlan& plan, c
     return cudaGetLastError();                                                                     \
   }
   B200SHA3_FEWBLOCK_SHAPES(X)
+#undef X
+  return cudaErrorNotSupported;
+}
+
+}  // namespace b200sha3
+
+namespace b200sha3 {
+
+bool manyblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes) {
+  if (msg_len % 8 != 0 || digest_bytes % 4 != 0 || msg_len < 8u * static_cast<uint64_t>(rate_lanes) ||
+      msg_len >= (1ull << 31)) {
+    return false;
+  }
+  const int ow = static_cast<int>(digest_bytes / 4);
+#define X(RL, OW) \
+  if (rate_lanes == RL && ow == OW) return true;
+  B200SHA3_MANYBLOCK_SHAPES(X)
+#undef X
+  return false;
+}
+
+// Equal-length messages of whole lanes, 16-byte aligned data and digests, whole-byte output.
+cudaError_t launch_hash_manyblock(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream) {
+  if (!manyblock_supported(plan.rate_lanes, args.fixed_len, args.digest_bytes) || args.offsets || args.lengths ||
+      args.order || !args.aligned8 || args.last_mask != 0xffu) {
+    return cudaErrorNotSupported;
+  }
+  const int threads = plan.block_threads > 0 ? plan.block_threads : 128;
+  const uint64_t blocks = (args.count + threads - 1) / threads;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > 0x7fffffffull) return cudaErrorInvalidConfiguration;
+  const int ow = static_cast<int>(args.digest_bytes / 4);
+  const uint32_t ml = static_cast<uint32_t>(args.fixed_len / 8);
+#define X(RL, OW)                                                                            \
+  if (plan.rate_lanes == RL && ow == OW) {                                                   \
+    hash_manyblock_kernel<RL, OW><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(    \
+        args.data, args.digests, args.count, args.head, ml);                                 \
+    return cudaGetLastError();                                                               \
+  }
+  B200SHA3_MANYBLOCK_SHAPES(X)
 #undef X
   return cudaErrorNotSupported;
 }

@@ -73,6 +73,10 @@ bool oneblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes)
 // cfg2 / cfg3; 16-byte aligned buffers, whole-byte output.  cudaErrorNotSupported otherwise.
 cudaError_t launch_hash_fewblock(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
 bool fewblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
+// The same round sequence with the message length a run-time value (same file): equal-length
+// messages of any whole number of lanes at or above the rate, digest within one block.
+cudaError_t launch_hash_manyblock(const HashArgs& args, const LaunchPlan& plan, cudaStream_t stream);
+bool manyblock_supported(int rate_lanes, uint64_t msg_len, uint64_t digest_bytes);
 
 // Variable-length batches made of single-block messages only (kernel_short.cu), input order; for
 // callers that KNOW the batch is all-short (the host entries).  Returns at once if the "long" flag

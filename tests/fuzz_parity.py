@@ -67,6 +67,8 @@ def main():
                 n = int(rng.choice([128, 256, 512, 1024])) if alg < 4 else 64
                 bits = 0 if alg < 4 else int(rng.choice([2048, 4096, 2045]))
                 n += int(rng.choice([0, 0, 0, 8, -8]))
+                if rng.random() < 0.3:  # any whole number of lanes (hash_manyblock_kernel when >= rate)
+                    n = 8 * int(rng.integers(1, 6 * rate // 8 + 2))
                 entry += "_shape"
             fixed = rng.integers(0, 256, max(count * n, 1) + 16, dtype=np.uint8)
             expect = oracle.hash_batch(alg, fixed, fixed_len=n, count=count, xof_bits=bits, workers=8)

@@ -156,7 +156,8 @@ def test_selected_kernel_names():
     assert selected_kernel("sha3_256", 64) == "hash_oneblock_kernel<17,8,8>"
     assert selected_kernel("sha3_256", 10) == "hash_short_fixed_kernel<17,8>"
     assert selected_kernel("sha3_512", 1024) == "hash_fewblock_kernel<9,128,16>"  # static multi-block shape
-    assert selected_kernel("sha3_512", 1032) == "hash_generic_kernel<9>"
+    assert selected_kernel("sha3_512", 1032) == "hash_manyblock_kernel<9,16>"     # any whole number of lanes >= rate
+    assert selected_kernel("sha3_512", 1030) == "hash_generic_kernel<9>"
     assert selected_kernel("shake256", 64, 4096) == "hash_fewblock_kernel<17,8,128>"
     assert selected_kernel("shake128", 64, 1023) == "hash_generic_kernel<21>"     # odd bits: masked tail
     assert selected_kernel("shake128", 64, 1024) == "hash_oneblock_kernel<21,8,32>"
@@ -167,4 +168,5 @@ def test_selected_kernel_names():
     assert selected_kernel("sha3_256", 1 << 20, count=1024) == "hash_warp_kernel"
     assert selected_kernel("sha3_256", None, count=100) == "hash_warp_kernel"
     assert selected_kernel("sha3_256", 64, count=100) == "hash_oneblock_kernel<17,8,8>"   # single block
-    assert selected_kernel("sha3_256", 1 << 20, count=1 << 14) == "hash_generic_kernel<17>"
+    assert selected_kernel("sha3_256", 1 << 20, count=1 << 14) == "hash_manyblock_kernel<17,8>"
+    assert selected_kernel("sha3_256", (1 << 20) + 1, count=1 << 14) == "hash_generic_kernel<17>"

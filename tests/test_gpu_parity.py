@@ -266,8 +266,8 @@ def test_fewblock_shapes(oracle, algorithm, msg_len, bits):
     # one message, and a count that leaves the last block of threads almost empty
     for n in (1, 129):
         assert (forced.hash_fixed(algorithm, dev, msg_len, n, bits).cpu().numpy() == expect[:n]).all()
-    with pytest.raises(EngineError):  # no such shape
-        forced.hash_fixed(algorithm, dev[:count * (msg_len - 8)].contiguous(), msg_len - 8, count, bits)
+    with pytest.raises(EngineError):  # not a whole number of lanes: neither the static nor the run-time-length form
+        forced.hash_fixed(algorithm, dev[:count * (msg_len - 4)].contiguous(), msg_len - 4, count, bits)
     # a buffer that is only 8-byte aligned: refused when forced, the generic kernel under AUTO
     shifted = torch.empty(host.size + 8, dtype=torch.uint8, device="cuda")[8:]
     shifted.copy_(dev)
@@ -279,6 +279,36 @@ def test_fewblock_shapes(oracle, algorithm, msg_len, bits):
             forced.hash_fixed(algorithm, dev, msg_len, count, bits - 3)
         odd = oracle.hash_batch(algorithm, host, fixed_len=msg_len, count=count, xof_bits=bits - 3, workers=4)
         assert (auto.hash_fixed(algorithm, dev, msg_len, count, bits - 3).cpu().numpy() == odd).all()
+
+
+@pytest.mark.parametrize("algorithm,bits", [(0, 0), (1, 0), (2, 0), (3, 0), (4, 128), (4, 256), (4, 512),
+                                            (5, 128), (5, 256), (5, 512)])
+def test_manyblock_every_length(oracle, algorithm, bits):
+    """The run-time-length form of the few-block kernel (hash_manyblock_kernel): equal-length
+    messages of every whole number of lanes from the rate to just past three rate blocks -- every
+    case of the final-block jump table with one, two and three whole blocks in front -- forced,
+    vs the oracle; plus two long shapes, and the same batches under KERNEL_AUTO."""
+    import torch
+    from paper_1902_05320_b200 import Engine, EngineError, rate_bytes, selected_kernel
+    from paper_1902_05320_b200.engine import FLAG_NO_WARP_KERNEL, KERNEL_FEWBLOCK
+    rate = rate_bytes(algorithm)
+    count = 131
+    forced, auto = Engine(kernel=KERNEL_FEWBLOCK), Engine(flags=FLAG_NO_WARP_KERNEL)
+    lengths = list(range(rate, 3 * rate + 17, 8)) + [5000 - 5000 % 8, 16 * rate]
+    for msg_len in lengths:
+        host = oracle.generate_workload(count * msg_len, msg_len, seed=29)
+        dev = torch.from_numpy(host).cuda()
+        expect = oracle.hash_batch(algorithm, host, fixed_len=msg_len, count=count, xof_bits=bits, workers=4)
+        got = forced.hash_fixed(algorithm, dev, msg_len, count, bits)
+        assert (got.cpu().numpy() == expect).all(), msg_len
+        assert torch.equal(got, auto.hash_fixed(algorithm, dev, msg_len, count, bits)), msg_len
+        name = selected_kernel(algorithm, msg_len, bits, 1 << 20)
+        assert name.startswith("hash_manyblock_kernel<") or name.startswith("hash_fewblock_kernel<"), (msg_len, name)
+    # below the rate, or not a whole number of lanes: not this kernel's
+    for msg_len in (rate - 8, rate + 4):
+        host = oracle.generate_workload(count * msg_len, msg_len, seed=29)
+        with pytest.raises(EngineError):
+            forced.hash_fixed(algorithm, torch.from_numpy(host).cuda(), msg_len, count, bits)
 
 
 @pytest.mark.parametrize("algorithm", [4, 5])

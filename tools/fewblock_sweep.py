@@ -16,7 +16,10 @@ probe = Engine(device=0)
 peak, hz = probe.probe_pipe(2)
 rows = []
 shapes = [("shake128", 64, 2048), ("shake128", 64, 4096), ("shake256", 64, 2048), ("shake256", 64, 4096),
-          ("sha3_224", 256, 0), ("sha3_384", 128, 0), ("sha3_384", 256, 0), ("sha3_512", 128, 0), ("sha3_512", 1024, 0)]
+          ("sha3_224", 256, 0), ("sha3_384", 128, 0), ("sha3_384", 256, 0), ("sha3_512", 128, 0), ("sha3_512", 1024, 0),
+          # run-time-length form (hash_manyblock_kernel): lengths without a static instantiation
+          ("sha3_256", 136, 0), ("sha3_256", 200, 0), ("sha3_256", 1000, 0), ("sha3_224", 400, 0), ("sha3_384", 104, 0),
+          ("sha3_512", 200, 0), ("shake128", 1024, 256), ("shake256", 200, 512)]
 for alg, msg, bits in shapes:
     data = probe.generate_workload(count * msg, msg, seed=1)
     out = torch.empty((count, digest_bytes(alg, bits)), dtype=torch.uint8, device="cuda")
