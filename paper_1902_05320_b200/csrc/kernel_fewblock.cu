@@ -1,5 +1,8 @@
-// kernel_fewblock.cu -- equal-length MULTI-block shapes (cfg2 lengths at or above the rate, cfg3
-// outputs longer than the rate), one message per thread, everything about the shape static.
+// kernel_fewblock.cu -- equal-length MULTI-block batches, one message per thread:
+//   hash_fewblock_kernel<RL, ML, OW>   everything about the shape static (cfg2 lengths at or above
+//                                      the rate, cfg3 outputs longer than the rate)
+//   hash_manyblock_kernel<RL, OW>      the same round sequence with the message length a run-time
+//                                      value (any whole number of lanes at or above the rate)
 //
 // hash_into (proj/core/src/batch.cpp:15-25) for a batch whose messages are ML whole lanes and whose
 // digests are OW whole 32-bit words, both compile-time: NB = ML / RL full blocks are absorbed
@@ -49,13 +52,10 @@ __constant__ uint32_t kRoundConstWrap[50] = {
 // free), the state is unconstrained and lands in another bad one (79).  Copying SOME lanes
 // breaks the pattern: kCopyLanes was found by a search over random lane sets with that census
 // (most sets give <= 2; this one gives 0 for all four multi-block-output shapes).
-constexpr uint32_t kCopyLanes = 0x10b417u;  // lanes 0,1,2,4,10,12,13,15,20
-#ifdef B200SHA3_FEWBLOCK_COPY_MASK            // census / search builds
-#undef B200SHA3_FEWBLOCK_COPY_LANES
-#define B200SHA3_FEWBLOCK_COPY_LANES B200SHA3_FEWBLOCK_COPY_MASK
-#else
-#define B200SHA3_FEWBLOCK_COPY_LANES kCopyLanes
+#ifndef B200SHA3_FEWBLOCK_COPY_LANES  // the search builds of tools/fewblock_lane_search.sh pass other sets
+#define B200SHA3_FEWBLOCK_COPY_LANES 0x10b417u  // lanes 0, 1, 2, 4, 10, 12, 13, 15, 20
 #endif
+constexpr uint32_t kCopyLanes = B200SHA3_FEWBLOCK_COPY_LANES;
 __device__ __forceinline__ uint32_t copy_reg(uint32_t v, uint32_t one) {
   uint32_t t;
   asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(t) : "r"(v), "r"(one));
@@ -64,7 +64,7 @@ __device__ __forceinline__ uint32_t copy_reg(uint32_t v, uint32_t one) {
 // lane j of the state as (lo, hi), through copies if the lane is in the set (j is a
 // compile-time value after unrolling)
 __device__ __forceinline__ uint2 lane_out(const State& a, int j, uint32_t one) {
-  const bool c = ((B200SHA3_FEWBLOCK_COPY_LANES >> j) & 1u) != 0u;
+  const bool c = ((kCopyLanes >> j) & 1u) != 0u;
   return make_uint2(c ? copy_reg(a.lo[j], one) : a.lo[j], c ? copy_reg(a.hi[j], one) : a.hi[j]);
 }
 __device__ __forceinline__ void store2(uint8_t* w, const State& a, int j, uint32_t one) {
