@@ -1,7 +1,8 @@
 // kernel_ragged.cu -- ONE launch for a variable-length batch whose shape is known on the device
 // only: the body of hash_short_kernel (kernel_short.cu) when the classification pass found
 // nothing but single-block messages, the body of hash_generic_kernel (kernel_generic.cu)
-// otherwise -- a kernel-uniform branch on the "long" flag word.
+// otherwise -- a kernel-uniform branch on the "long" flag word.  In a mixed batch the warps that hold
+// nothing but single-block messages (the tail of the bucketing order) take the short body as well.
 //
 // Before, both kernels were launched and one of them returned at once; the one that returned
 // still had its whole grid dispatched (131 072 empty blocks for 2^24 messages: 70 us, 1.7 % of
@@ -25,27 +26,32 @@ hash_ragged_kernel(const HashArgs args) {
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (tid >= args.count) return;
   const bool aligned8 = *args.unaligned_flag == 0u;
-  if (*args.long_flag == 0u) {
-    // every message is a single block (kernel_short.cu): input order and the predicated absorb on
-    // 8-byte aligned starts, word-count order and the jump-table absorb otherwise
-    const bool sorted = args.order != nullptr && !aligned8;
-    const uint64_t m = sorted ? static_cast<uint64_t>(args.order[tid]) : tid;
+  const bool all_short = *args.long_flag == 0u;
+  // An all-short batch with 8-byte aligned starts is taken in input order (the scatter pass
+  // returned at once and left no order); everything else walks the bucketing order.
+  const bool ordered = args.order != nullptr && !(all_short && aligned8);
+  const uint64_t m = ordered ? static_cast<uint64_t>(args.order[tid]) : tid;
+  const uint64_t length = args.lengths[m];
+  // The short body (kernel_short.cu) for a batch of single-block messages -- and, in a MIXED batch
+  // (keys and records: some messages below the rate, some above), for every warp that holds
+  // nothing else: the bucketing order puts the single-block messages last, sorted by word count,
+  // so whole warps of them exist (4440 instead of 4755 instructions per message).  Predicated
+  // absorb on 8-byte aligned starts, word-count order and the jump-table absorb otherwise.
+  if (all_short || __all_sync(__activemask(), length < 8u * RL)) {
     const uint8_t* p = args.data + args.offsets[m];
-    const uint32_t len = static_cast<uint32_t>(args.lengths[m]);  // < 8 * RL
     State a;
     state_zero(a);
-    if (sorted) {
-      absorb_tail_uniform_unaligned<RL>(a, p, len, args.head);
+    if (ordered && !aligned8) {
+      absorb_tail_uniform_unaligned<RL>(a, p, static_cast<uint32_t>(length), args.head);
     } else {
-      absorb_tail<RL>(a, p, len, args.head, aligned8, /*ragged=*/true);
+      absorb_tail<RL>(a, p, static_cast<uint32_t>(length), args.head, aligned8, /*ragged=*/true);
     }
     keccak_f1600<23, 0u>(a);  // peeled 1 + 7x3 + 2
     emit_block<RL>(a, args.digests + m * (4u * OW), 4u * OW);
     return;
   }
-  const uint64_t m = args.order ? static_cast<uint64_t>(args.order[tid]) : tid;
   const bool ragged = *args.ragged_flag != 0u;
-  hash_message<RL, kRaggedUnroll, 0u>(args.data + args.offsets[m], args.lengths[m],
+  hash_message<RL, kRaggedUnroll, 0u>(args.data + args.offsets[m], length,
                                       args.digests + m * args.digest_bytes, args.digest_bytes, args.head,
                                       args.last_mask, aligned8, ragged);
 }
