@@ -51,9 +51,9 @@ hash_ragged_kernel(const HashArgs args) {
     return;
   }
   const bool ragged = *args.ragged_flag != 0u;
-  hash_message<RL, kRaggedUnroll, 0u>(args.data + args.offsets[m], length,
-                                      args.digests + m * args.digest_bytes, args.digest_bytes, args.head,
-                                      args.last_mask, aligned8, ragged);
+  // digest = 4 OW bytes, whole bytes (launch_hash_ragged checks): the static-output form
+  hash_message_static_out<RL, OW, kRaggedUnroll, 0u>(args.data + args.offsets[m], length,
+                                                     args.digests + m * (4u * OW), args.head, aligned8, ragged);
 }
 
 template <int RL, int OW>

@@ -342,6 +342,39 @@ __device__ __forceinline__ void hash_message(const uint8_t* p, uint64_t len, uin
   }
 }
 
+// The same for a digest of OW whole 32-bit words that fits one block, OW a compile-time value
+// (the four hashes; short SHAKE outputs): no squeeze loop, and the finishing permutation is the
+// peeled form (1 + 7x3 + 2) followed by a static store, so ptxas drops the work of the last two
+// rounds on the lanes nobody reads -- ~120 instructions per message, which is what a message of
+// two or three blocks notices.
+template <int RL, int OW, int UNROLL, uint32_t FMA_MASK>
+__device__ __forceinline__ void hash_message_static_out(const uint8_t* p, uint64_t len, uint8_t* out,
+                                                        uint32_t head, bool aligned8, bool ragged) {
+  static_assert(OW <= 2 * RL, "digest must fit one block");
+  constexpr uint32_t R = 8u * RL;
+  State a;
+  state_zero(a);
+  uint64_t left_in = len;
+  if (aligned8) {
+    while (left_in >= R) {
+      absorb_lanes_aligned<RL>(a, p, RL);
+      keccak_f1600<UNROLL, FMA_MASK>(a);
+      p += R;
+      left_in -= R;
+    }
+  } else {
+    while (left_in >= R) {
+      absorb_words_unaligned<RL>(a, p, 2 * RL);
+      keccak_f1600<UNROLL, FMA_MASK>(a);
+      p += R;
+      left_in -= R;
+    }
+  }
+  absorb_tail<RL>(a, p, static_cast<uint32_t>(left_in), head, aligned8, ragged);
+  keccak_f1600<23, FMA_MASK>(a);
+  emit_block<RL>(a, out, 4u * OW);
+}
+
 // ---------------------------------------------------------------------------
 // Byte-granular pieces for the incremental (streaming) entry points: the state
 // carries a byte position like SpongeHasher::pos_ (sponge.hpp:60-63).
