@@ -533,14 +533,18 @@ def main():
         # ways at once on two streams, no hashing (tools/microbench/pcie_duplex.cu is the
         # stand-alone form).  H2D runs slower under opposite traffic than alone.
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        with torch.cuda.stream(s_in):
-            data[:e2e_count * MSG_LEN].copy_(host_in, non_blocking=True)
-        with torch.cuda.stream(s_out):
-            host_out.copy_(digests.view(-1)[:e2e_count * DIGEST_BYTES], non_blocking=True)
-        torch.cuda.synchronize()
-        duplex_seconds = max_over_ranks(time.perf_counter() - t0)
+        duplex_seconds = None
+        for _ in range(2):          # the faster of two passes
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(s_in):
+                data[:e2e_count * MSG_LEN].copy_(host_in, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                host_out.copy_(digests.view(-1)[:e2e_count * DIGEST_BYTES], non_blocking=True)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            duplex_seconds = dt if duplex_seconds is None else min(duplex_seconds, dt)
+        duplex_seconds = max_over_ranks(duplex_seconds)
         e2e_total = e2e_count * world if e2e_count != count else total
         e2e = {"value": e2e_total * e2e_steps / e2e_seconds, "unit": "hashes/s",
                "h2d_bytes_per_step": e2e_total * MSG_LEN, "d2h_bytes_per_step": e2e_total * DIGEST_BYTES,
