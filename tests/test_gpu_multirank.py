@@ -82,3 +82,23 @@ def test_nccl_branch_when_two_devices_are_visible(single):
     assert "validation_only" not in line
     _check_sharded(line, single, 2)
     assert line["digest_gather"]["checksum_matches"] is True and line["digest_gather"]["backend"] == "nccl"
+
+
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_variable_length_batch_sharded_by_block_count(ranks):
+    """SURVEY.md 8(e), variable-length half: contiguous ranges balanced by cumulative block count,
+    each rank hashing its range with the CUDA path under a process group; the concatenation is
+    the unsharded result and the ranges carry near-equal work."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           str(ROOT / "tests" / "integration" / "multirank_ragged.py"), "30000"]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=str(ROOT), env=env)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["ranks"] == ranks and rec["sharded_equals_unsharded"] is True and rec["oracle_sample_ok"] is True
+    assert sum(c for _, c in rec["ranges"]) == 30000
+    work = rec["blocks_per_rank"]
+    assert max(work) - min(work) <= 2 * (200000 // 136 + 1)      # within a heaviest message or two
